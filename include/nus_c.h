@@ -1,0 +1,168 @@
+/* nus_c.h — C-ABI of the B200-native MTNUFFT hot path (libnus_b200.so).
+ *
+ * This is the drop-in boundary: plain pointers and sizes, opaque handles,
+ * status codes, no C++ or torch types.  It replaces the reference's
+ * in-process C++ calls on the MTNUFFT path (paths relative to
+ * /root/reference/proj):
+ *
+ *   nus_plan_*            NufftPlan            include/nuspectral/nufft.hpp:31-76, src/nufft.cpp:56-187
+ *   nus_ndft_direct       ndft_direct          include/nuspectral/nufft.hpp:16-18, src/nufft.cpp:36-54
+ *   nus_dpss              dpss_uniform         include/nuspectral/tapers.hpp:22-23, src/tapers.cpp:31-79
+ *   nus_tridiagonal_eigen tridiagonal_eigen    include/nuspectral/eig.hpp:30-32,     src/eig.cpp:572-610
+ *   nus_signal_band_quadform  signal_band_kernel + KernelMatrix::quadratic_form
+ *                                              include/nuspectral/kernels.hpp:38,60, src/kernels.cpp:28-37,100-115
+ *   nus_gpss_interpolated gpss_interpolated    include/nuspectral/tapers.hpp:86-87, src/tapers.cpp:146-182
+ *   nus_mtnufft_*         MtnufftEstimator / eigencoefficients / estimate_mtnufft
+ *                                              include/nuspectral/estimators.hpp:39-62,133-137,
+ *                                              src/estimators.cpp:91-122,261-270, src/nufft.cpp:194-227
+ *
+ * Conventions
+ *  - Complex data is interleaved (re, im) in the plan's precision.
+ *  - Host entry points take host pointers (std::vector semantics of the
+ *    reference).  *_device entry points take device pointers plus a
+ *    cudaStream_t passed as void* and never synchronise.
+ *  - Every function returns a status; it never throws.  nus_last_error()
+ *    returns the calling thread's last message.  The status codes map 1:1 to
+ *    the reference's exception types (errors.hpp:9-49, std::invalid_argument).
+ *  - There is no CPU fallback: without a usable sm_100 device every compute
+ *    entry point fails with NUS_ERR_NO_DEVICE.
+ */
+#ifndef NUS_C_H
+#define NUS_C_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum nus_status {
+  NUS_OK = 0,
+  NUS_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+  NUS_ERR_PLAN_MISMATCH = 2,    /* nuspectral::PlanMismatch */
+  NUS_ERR_BAND_RANGE = 3,       /* nuspectral::BandRangeError */
+  NUS_ERR_EXTRAPOLATION = 4,    /* nuspectral::ExtrapolationError */
+  NUS_ERR_NUMERIC = 5,          /* nuspectral::Error (numeric failure) */
+  NUS_ERR_CUDA = 6,             /* CUDA / cuFFT runtime failure */
+  NUS_ERR_OUT_OF_MEMORY = 7,
+  NUS_ERR_NO_DEVICE = 8
+};
+
+enum nus_path_policy { NUS_AUTO_SELECT = 0, NUS_FORCE_FAST = 1, NUS_FORCE_DIRECT = 2 };
+enum nus_path { NUS_PATH_DIRECT = 0, NUS_PATH_FAST = 1 };
+enum nus_precision { NUS_F64 = 0, NUS_F32 = 1 };
+
+typedef struct nus_plan_s* nus_plan_t;
+typedef struct nus_mtnufft_s* nus_mtnufft_t;
+
+typedef struct {
+  int64_t n_samples;
+  int64_t n_centers;
+  double epsilon;
+  int32_t oversampling;
+  int32_t path;            /* enum nus_path */
+  int32_t centers_uniform; /* nufft.cpp:23-32 */
+  int32_t precision;       /* enum nus_precision */
+  int64_t spread_width;    /* w; 2w cells per sample (nufft.cpp:90-92) */
+  int64_t mr;              /* oversampled grid (nufft.cpp:103-104), 0 on the direct path */
+  double tau;              /* Gaussian width (nufft.cpp:105-108) */
+  double df;               /* centre spacing */
+  double fshift;           /* f0 + (I/2) df */
+} nus_plan_info_t;
+
+const char* nus_last_error(void);
+/* Library/device facts: device count, compute capability, build string. */
+int nus_device_info(int device, int32_t* cc_major, int32_t* cc_minor, int32_t* sm_count,
+                    int64_t* total_mem);
+/* Number of this library's kernels launched so far (process-wide). */
+int64_t nus_kernel_launch_count(void);
+
+/* ---- NufftPlan (nufft.hpp:31-76) ---------------------------------------- */
+int nus_plan_create(const double* times, int64_t n, const double* centers, int64_t n_centers,
+                    double epsilon, int32_t policy, int32_t oversampling, int32_t precision,
+                    int32_t device, nus_plan_t* out);
+int nus_plan_destroy(nus_plan_t plan);
+int nus_plan_info(nus_plan_t plan, nus_plan_info_t* info);
+/* Reference first_cell_ (j0 = floor(x*Mr/2pi) - w + 1 per sample, nufft.cpp:118-122), bit-exact. */
+int nus_plan_first_cells(nus_plan_t plan, int64_t* out_host);
+/* Stable order of samples by start cell (j0 mod Mr) used by the spreading kernel. */
+int nus_plan_sort_order(nus_plan_t plan, int32_t* perm_host);
+/* NufftPlan::execute on one complex vector (host in/out, interleaved fp64). */
+int nus_plan_execute(nus_plan_t plan, const double* y_host, int64_t n_y, double* out_host);
+/* Batched device execute: y_dev [batch][n] complex, out_dev [batch][I] complex (plan precision). */
+int nus_plan_execute_device(nus_plan_t plan, const void* y_dev, int64_t batch, void* out_dev,
+                            void* stream);
+
+/* Direct NUDFT oracle path (nufft.cpp:36-54) on the device, fp64. */
+int nus_ndft_direct(const double* times, int64_t n, const double* y_host, const double* centers,
+                    int64_t n_centers, int32_t device, double* out_host);
+
+/* ---- tapers (tapers.hpp) -------------------------------------------------- */
+/* Top-k eigenpairs of the commuting tridiagonal (tapers.cpp:40-52); vectors K x n unit norm,
+ * largest-|v| entry positive (eig.cpp:281-289).  eigenvalues / concentrations may be NULL. */
+int nus_dpss(int64_t n, double time_half_bandwidth, int64_t k, int32_t device, double* tapers_host,
+             double* eigenvalues_host, double* concentrations_host);
+int nus_tridiagonal_eigen(const double* diag, const double* offdiag, int64_t n, int64_t k,
+                          int32_t device, double* values, double* vectors, double* residuals);
+/* q_k = w_k^T R(B) w_k for K weight rows over rows [row_begin,row_end) of R(B) (pass 0,n for all). */
+int nus_signal_band_quadform(const double* times, int64_t n, double f_max, const double* w_host,
+                             int64_t k, int64_t row_begin, int64_t row_end, int32_t device,
+                             double* q_host);
+/* Un-normalised interpolated DPSS: spline of dpss_uniform(n, f_w*h*n, k) at t (tapers.cpp:156-174). */
+int nus_taper_spline(const double* times, int64_t n, double f_max, double f_w, int64_t k,
+                     int32_t device, double* w_host);
+/* Full gpss_interpolated: spline + R(B) normalisation to w^T R(B) w = 2 f_w. */
+int nus_gpss_interpolated(const double* times, int64_t n, double f_max, double f_w, int64_t k,
+                          int32_t device, double* weights_host);
+
+/* ---- MtnufftEstimator (estimators.hpp:39-62) -------------------------------
+ * channels independent series share n, the centres, K and epsilon.
+ * times: [channels][n].  tapers: NULL -> computed on the GPU (gpss_interpolated per
+ * channel), else injected normalised weights [channels][K][n] (Oracle-B style).
+ * The setup (DPSS, spline, R(B) norm, bins, sort) runs on the device. */
+typedef struct {
+  int64_t channels;
+  int64_t n;
+  int64_t n_centers;
+  int64_t k_tapers;
+  double f_max;
+  double f_w;
+  double epsilon;
+  int32_t policy;
+  int32_t precision;
+  int32_t device;
+  int32_t reserved;
+} nus_mtnufft_config_t;
+
+int nus_mtnufft_create(const nus_mtnufft_config_t* cfg, const double* times, const double* centers,
+                       const double* tapers, nus_mtnufft_t* out);
+int nus_mtnufft_destroy(nus_mtnufft_t est);
+int nus_mtnufft_plan_info(nus_mtnufft_t est, nus_plan_info_t* info);
+/* Normalised taper weights [channels][K][n] (fp64, time order). */
+int nus_mtnufft_tapers(nus_mtnufft_t est, double* out_host);
+/* Setup timings in ms: [dpss, spline, normalise, plan(bins+sort+tables), total]. */
+int nus_mtnufft_setup_ms(nus_mtnufft_t est, double* out5);
+/* estimate(): x [channels][n] fp64 host -> power [channels][I] fp64 host. */
+int nus_mtnufft_estimate(nus_mtnufft_t est, const double* x_host, double* power_host);
+/* eigencoefficients(): -> J [channels][K][I] complex fp64 host (nufft.cpp:194-227). */
+int nus_mtnufft_eigencoefficients(nus_mtnufft_t est, const double* x_host, double* j_host);
+/* Device-resident estimate.  x_dev: [channels][n] of x_dtype (0 f64, 1 f32); power_dev:
+ * [channels][I] in the plan precision; j_dev optional [channels][K][I] complex. */
+int nus_mtnufft_estimate_device(nus_mtnufft_t est, const void* x_dev, int32_t x_dtype,
+                                void* power_dev, void* j_dev, void* stream);
+/* Sample-split building blocks.  spread: samples [s0,s1) (time order) of every
+ * channel into grid_dev [channels][k_pad][Mr] complex (tapers >= K left untouched);
+ * transform: FFT + deconvolve/crop + sum_k |J|^2 / divisor of tapers [k0,k1) held in grid_dev
+ * rows 0..k1-k0-1 (one channel), written to (or added into, accumulate != 0) power_dev. */
+int nus_mtnufft_spread_device(nus_mtnufft_t est, const void* x_dev, int32_t x_dtype, int64_t s0,
+                              int64_t s1, void* grid_dev, int64_t k_pad, void* stream);
+int nus_mtnufft_transform_device(nus_mtnufft_t est, void* grid_dev, int64_t k0, int64_t k1,
+                                 double divisor, int32_t accumulate, void* power_dev, void* stream);
+/* Algorithmic bytes of one estimate (SURVEY §8d model) and of its spreading kernel. */
+int nus_mtnufft_bytes_model(nus_mtnufft_t est, int32_t x_dtype, double* total, double* spread,
+                            double* fft, double* crop);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NUS_C_H */

@@ -1,0 +1,30 @@
+// Estimator object shared by mtnufft.cu and capi.cu.
+#pragma once
+
+#include "nus_internal.cuh"
+
+namespace nus {
+
+struct Estimator {
+  nus_mtnufft_config_t cfg{};
+  std::unique_ptr<Plan> plan;
+  DeviceBuffer tapers_time;    // fp64 [C][K][n], time order (normalised)
+  DeviceBuffer tapers_sorted;  // plan precision [C][K][n], start-cell order
+  DeviceBuffer grid;           // [C][K][Mr] complex, plan precision
+  DeviceBuffer x_stage, p_stage, j_stage;  // host-API staging
+  double setup_ms[5] = {0, 0, 0, 0, 0};
+  std::mutex mu;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream();
+  ~Estimator();
+};
+
+std::unique_ptr<Estimator> estimator_create(const nus_mtnufft_config_t& cfg, const double* times,
+                                            const double* centers, const double* tapers);
+void estimator_run(Estimator& est, const void* x_dev, int x_dtype, void* power_dev, bool power_f64,
+                   void* j_dev, cudaStream_t s);
+void estimator_estimate_host(Estimator& est, const double* x, double* power, double* j);
+void estimator_bytes(const Estimator& est, int x_dtype, double* total, double* spread, double* fft,
+                     double* crop);
+
+}  // namespace nus

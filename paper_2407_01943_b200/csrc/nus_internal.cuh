@@ -1,0 +1,225 @@
+// Internal declarations shared by the libnus_b200 translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cufft.h>
+
+#include <atomic>
+#include <cstdint>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "nus_c.h"
+
+namespace nus {
+
+constexpr double kPi = 3.14159265358979323846;
+constexpr double kTwoPi = 2.0 * 3.14159265358979323846;
+
+// Status-carrying exception used inside the library; converted to a status
+// code at the C-ABI boundary (capi.cu) and never crosses it.
+struct Failure : std::runtime_error {
+  int code;
+  Failure(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Failure(code, msg); }
+inline void require(bool ok, const std::string& msg) {
+  if (!ok) fail(NUS_ERR_INVALID_ARGUMENT, msg);
+}
+
+void cuda_check(cudaError_t e, const char* what);
+void cufft_check(cufftResult r, const char* what);
+#define NUS_CUDA(x) ::nus::cuda_check((x), #x)
+#define NUS_CUFFT(x) ::nus::cufft_check((x), #x)
+
+// Count of our own kernel launches (the bench reports it as gpu_launches).
+extern std::atomic<int64_t> g_launches;
+inline void note_launch(int64_t k = 1) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+void check_launch(const char* what);
+
+// Selects `device` for the calling thread and verifies it is an sm_100 part.
+void use_device(int device);
+
+// RAII device buffer.
+struct DeviceBuffer {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  DeviceBuffer() = default;
+  explicit DeviceBuffer(size_t b) { alloc(b); }
+  DeviceBuffer(const DeviceBuffer&) = delete;
+  DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+  DeviceBuffer(DeviceBuffer&& o) noexcept : ptr(o.ptr), bytes(o.bytes) { o.ptr = nullptr; o.bytes = 0; }
+  DeviceBuffer& operator=(DeviceBuffer&& o) noexcept {
+    if (this != &o) { release(); ptr = o.ptr; bytes = o.bytes; o.ptr = nullptr; o.bytes = 0; }
+    return *this;
+  }
+  ~DeviceBuffer() { release(); }
+  void alloc(size_t b);
+  void release();
+  template <class T> T* as() const { return static_cast<T*>(ptr); }
+};
+
+// ---- plan ------------------------------------------------------------------
+
+// Per-grid NUFFT tables on the device, all indexed in start-cell-sorted order.
+struct PlanParams {
+  int64_t n = 0;          // samples per channel
+  int64_t nc = 0;         // centres I
+  int64_t channels = 1;
+  double eps = 0;
+  int oversampling = 2;
+  int path = NUS_PATH_FAST;
+  bool uniform = false;
+  int precision = NUS_F64;
+  int w = 0;              // spread width; support is 2w cells
+  int64_t mr = 0;
+  double tau = 0, f0 = 0, df = 0, fshift = 0;
+  int64_t mode_offset = 0;
+  double beta = 0;        // Gaussian exponent per cell^2: (2pi/Mr)^2 / (4 tau)
+  double deconv_norm = 0; // sqrt(pi/tau)/Mr
+};
+
+struct SpreadTables {
+  int tile = 512;               // cells per spreading tile
+  int64_t ntiles = 0;
+  DeviceBuffer start;           // int32 [C][n] start cell s = j0 mod Mr (sorted)
+  DeviceBuffer perm;            // int32 [C][n] original sample index of sorted point
+  DeviceBuffer frac;            // real  [C][n] fractional cell offset in [0,1)
+  DeviceBuffer prephase;        // real2 [C][n] e^{-i 2pi fshift t}
+  DeviceBuffer tile_range;      // int32 [C][ntiles+1][2]: point range of tile (lo, hi)
+  DeviceBuffer wrap_lo;         // int32 [C]: first sorted point whose support wraps into tile 0
+  DeviceBuffer deconv;          // real  [I]
+  DeviceBuffer first_cell;      // int64 [C][n] reference j0, time order (kept for parity queries)
+};
+
+class FftCache {
+ public:
+  cufftHandle get(int64_t mr, int64_t batch, int precision);
+  ~FftCache();
+ private:
+  struct Entry { int64_t mr, batch; int precision; cufftHandle h; };
+  std::vector<Entry> entries_;
+};
+
+struct Plan {
+  PlanParams p;
+  int device = 0;
+  std::vector<double> times;    // host copy, time order [C][n]
+  std::vector<double> centers;
+  DeviceBuffer d_times;         // fp64 [C][n]
+  DeviceBuffer d_centers;       // fp64 [I]
+  SpreadTables tab;
+  FftCache fft;
+  std::mutex mu;                // serialises use of the default workspace + cuFFT plans
+  DeviceBuffer work;            // default grid workspace
+};
+
+void plan_validate_and_select(PlanParams& p, const double* centers, int64_t nc, double eps,
+                              int policy, int oversampling);
+void plan_build_tables(Plan& plan, cudaStream_t s);
+std::unique_ptr<Plan> plan_create(const double* times, int64_t channels, int64_t n,
+                                  const double* centers, int64_t nc, double eps, int policy,
+                                  int oversampling, int precision, int device);
+
+// Spreads K taper-weighted copies of x (sorted-order tapers; nullptr tapers = weight 1 and
+// x complex) onto grid [C][kpad][Mr].  Samples [s0, s1) in time order only.
+struct SpreadArgs {
+  const void* x = nullptr;   // [C][n] real (x_dtype) or complex when x_complex
+  int x_dtype = 0;           // 0 f64, 1 f32
+  bool x_complex = false;
+  const void* tapers = nullptr;  // [C][K][n] sorted-order real (plan precision)
+  int64_t k = 1;
+  int64_t kpad = 1;
+  int64_t s0 = 0, s1 = -1;
+  void* grid = nullptr;
+};
+void launch_spread(const Plan& plan, const SpreadArgs& a, cudaStream_t s);
+
+// FFT of rows [C][kpad][Mr] (first k rows per channel are transformed), then crop:
+// optional J [C][k][I] = deconv * B[bin] and power [C][I] (+)= sum_k |J|^2 / divisor.
+void run_transform(Plan& plan, void* grid, int64_t k, int64_t kpad, void* j_out, void* power,
+                   bool power_f64, double divisor, bool accumulate, cudaStream_t s);
+
+void launch_ndft_direct(const double* d_t, int64_t n, const void* d_y, bool y_f32,
+                        const double* d_c, int64_t nc, void* d_out, bool out_f32, int64_t batch,
+                        cudaStream_t s);
+
+// ---- tapers ----------------------------------------------------------------
+
+struct DpssResult {
+  std::vector<double> values;  // K descending
+};
+// vectors on device: d_vec [K][n] fp64
+DpssResult dpss_device(int64_t n, double tw, int64_t k, double* d_vec, cudaStream_t s);
+DpssResult tridiag_top_device(const double* d_diag, const double* d_off, int64_t n, int64_t k,
+                              double* d_vec, cudaStream_t s);
+void dpss_concentrations(int64_t n, double tw, int64_t k, const double* d_vec, double* conc,
+                         cudaStream_t s);
+// Interpolates K DPSS rows (knots t0 + h i) at times d_t -> d_w [K][n].
+void spline_uniform_device(const double* d_t, int64_t n, const double* d_y, int64_t k,
+                           double* d_w, cudaStream_t s);
+void quadform_device(const double* d_t, int64_t n, double f_max, const double* d_w, int64_t k,
+                     int64_t row0, int64_t row1, double* q_host, cudaStream_t s);
+// Full gpss_interpolated for one grid: d_w [K][n] normalised; timings optional.
+void gpss_interpolated_device(const double* d_t, const double* h_t, int64_t n, double f_max,
+                              double f_w, int64_t k, double* d_w, cudaStream_t s,
+                              double* ms_dpss = nullptr, double* ms_spline = nullptr,
+                              double* ms_norm = nullptr);
+
+__host__ __device__ inline int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }
+__host__ __device__ inline int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+// ---- double-double helpers ---------------------------------------------------
+
+struct dd { double hi, lo; };
+
+__host__ __device__ inline dd dd_two_sum(double a, double b) {
+  double s = a + b;
+  double bb = s - a;
+  double e = (a - (s - bb)) + (b - bb);
+  return {s, e};
+}
+__host__ __device__ inline dd dd_quick(double a, double b) {
+  double s = a + b;
+  return {s, b - (s - a)};
+}
+__device__ inline dd dd_add(dd a, dd b) {
+  dd s = dd_two_sum(a.hi, b.hi);
+  dd t = dd_two_sum(a.lo, b.lo);
+  s.lo += t.hi;
+  s = dd_quick(s.hi, s.lo);
+  s.lo += t.lo;
+  return dd_quick(s.hi, s.lo);
+}
+__device__ inline dd dd_neg(dd a) { return {-a.hi, -a.lo}; }
+__device__ inline dd dd_sub(dd a, dd b) { return dd_add(a, dd_neg(b)); }
+__device__ inline dd dd_mul(dd a, dd b) {
+  double p = a.hi * b.hi;
+  double e = fma(a.hi, b.hi, -p);
+  e = fma(a.hi, b.lo, e);
+  e = fma(a.lo, b.hi, e);
+  return dd_quick(p, e);
+}
+__device__ inline dd dd_mul_d(dd a, double b) {
+  double p = a.hi * b;
+  double e = fma(a.hi, b, -p);
+  e = fma(a.lo, b, e);
+  return dd_quick(p, e);
+}
+__device__ inline dd dd_div(dd a, dd b) {
+  double q1 = a.hi / b.hi;
+  dd r = dd_sub(a, dd_mul_d(b, q1));
+  double q2 = r.hi / b.hi;
+  r = dd_sub(r, dd_mul_d(b, q2));
+  double q3 = r.hi / b.hi;
+  dd q = dd_quick(q1, q2);
+  return dd_add(q, dd{q3, 0.0});
+}
+__device__ inline dd dd_from(double a) { return {a, 0.0}; }
+__device__ inline double dd_abs_hi(dd a) { return fabs(a.hi); }
+
+}  // namespace nus

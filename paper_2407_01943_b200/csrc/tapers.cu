@@ -1,0 +1,801 @@
+// Taper setup on the device: nominal-band DPSS, not-a-knot spline
+// interpolation to the sample times, and R(B)-metric normalisation.
+//
+// Reference (paths relative to /root/reference/proj):
+//   dpss_uniform       src/tapers.cpp:31-79   (matrix entries :40-52 reproduced exactly)
+//   tridiagonal_eigen  src/eig.cpp:572-610    (QL + inverse iteration; here: Sturm
+//                      multisection in fp64 + inverse iteration in double-double)
+//   canonical_sign     src/eig.cpp:281-289
+//   CubicSpline        src/eig.cpp:671-745    (not-a-knot; here: the uniform-knot
+//                      moment system solved by its exact two-sided recursive filter)
+//   signal_band_kernel + quadratic_form   src/kernels.cpp:16-19,28-37,100-115
+//                      (here: an O(N^2) tiled kernel without the dense matrix)
+//   gpss_interpolated  src/tapers.cpp:146-182
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cfloat>
+#include <chrono>
+#include <cmath>
+
+#include "nus_internal.cuh"
+
+namespace nus {
+
+namespace {
+
+// ---------------------------------------------------------------- Sturm counts
+
+// Each thread evaluates kProbes shift values (independent chains give ILP).
+constexpr int kProbes = 4;
+constexpr int kSturmThreads = 64;
+
+__global__ void sturm_multisect_kernel(const double* __restrict__ d, const double* __restrict__ e2,
+                                       int64_t n, const double* __restrict__ lo,
+                                       const double* __restrict__ hi, int probes_per_eig,
+                                       double pivmin, int32_t* __restrict__ counts) {
+  const int j = blockIdx.y;  // eigenvalue rank
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int p0 = t * kProbes;
+  if (p0 >= probes_per_eig) return;
+  const double a = lo[j], b = hi[j];
+  const double step = (b - a) / static_cast<double>(probes_per_eig + 1);
+  double lam[kProbes], q[kProbes];
+  int cnt[kProbes];
+#pragma unroll
+  for (int u = 0; u < kProbes; ++u) {
+    lam[u] = a + step * static_cast<double>(p0 + u + 1);
+    q[u] = d[0] - lam[u];
+    if (fabs(q[u]) < pivmin) q[u] = -pivmin;
+    cnt[u] = q[u] < 0.0 ? 1 : 0;
+  }
+  for (int64_t i = 1; i < n; ++i) {
+    const double di = d[i], ei = e2[i - 1];
+#pragma unroll
+    for (int u = 0; u < kProbes; ++u) {
+      double v = (di - lam[u]) - ei / q[u];
+      if (fabs(v) < pivmin) v = -pivmin;
+      q[u] = v;
+      cnt[u] += v < 0.0 ? 1 : 0;
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kProbes; ++u)
+    if (p0 + u < probes_per_eig) counts[j * probes_per_eig + p0 + u] = cnt[u];
+}
+
+__global__ void square_kernel(const double* __restrict__ e, int64_t m, double* __restrict__ e2) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < m) e2[i] = e[i] * e[i];
+}
+
+// ------------------------------------------------- inverse iteration (double-double)
+
+__device__ inline uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// One thread per eigenvector.  Each iteration solves (T - sigma I) x_new = x
+// with partial pivoting (the structure of src/eig.cpp:119-168) entirely in
+// double-double, storing the U factor rows (inverse pivot, u1, u2) in global
+// scratch for the back substitution.  x is renormalised between iterations.
+__global__ void inverse_iteration_dd_kernel(const double* __restrict__ d, const double* __restrict__ e,
+                                            int64_t n, const double* __restrict__ sigma_hi,
+                                            const double* __restrict__ sigma_lo, int iters,
+                                            double pivmin, dd* __restrict__ xs, dd* __restrict__ us,
+                                            double* __restrict__ norms) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= gridDim.x * blockDim.x) return;
+  const int64_t k_count = gridDim.x * blockDim.x;
+  (void)k_count;
+  dd* x = xs + static_cast<int64_t>(j) * n;
+  dd* u = us + static_cast<int64_t>(j) * n * 3;  // per row: inv u0, u1, u2
+  const dd sig = {sigma_hi[j], sigma_lo[j]};
+  // pseudo-random start vector in [-0.5, 0.5)
+  for (int64_t i = 0; i < n; ++i) {
+    const uint64_t r = mix64(0x9E3779B97F4A7C15ull * static_cast<uint64_t>(j + 1) + static_cast<uint64_t>(i));
+    x[i] = dd{static_cast<double>(r >> 11) * 0x1.0p-53 - 0.5, 0.0};
+  }
+  dd scale = {1.0, 0.0};
+  const dd pm = {pivmin, 0.0};
+  double final_norm = 1.0;
+  for (int it = 0; it < iters; ++it) {
+    if (n == 1) {
+      dd p = dd_sub(dd_from(d[0]), sig);
+      if (fabs(p.hi) < pivmin) p = p.hi < 0 ? dd_neg(pm) : pm;
+      x[0] = dd_div(dd_mul(x[0], scale), p);
+      final_norm = fabs(x[0].hi);
+      scale = dd_div(dd_from(1.0), dd_from(final_norm));
+      break;
+    }
+    // forward elimination
+    dd c0 = dd_sub(dd_from(d[0]), sig);
+    dd c1 = dd_from(e[0]);
+    dd c2 = dd_from(0.0);
+    dd xi = dd_mul(x[0], scale);
+    for (int64_t i = 0; i + 1 < n; ++i) {
+      const double sub = e[i];
+      const dd ddv = dd_sub(dd_from(d[i + 1]), sig);
+      const double sup = (i + 2 < n) ? e[i + 1] : 0.0;
+      dd xn = dd_mul(x[i + 1], scale);
+      if (fabs(sub) > fabs(c0.hi)) {
+        // pivot on the row below: row i <- (sub, dd, sup), swap rhs
+        const dd m = dd_div(c0, dd_from(sub));
+        u[3 * i] = dd_div(dd_from(1.0), dd_from(sub));
+        u[3 * i + 1] = ddv;
+        u[3 * i + 2] = dd_from(sup);
+        const dd tmp = xi;
+        x[i] = xn;
+        xi = dd_sub(tmp, dd_mul(m, xn));
+        c0 = dd_sub(c1, dd_mul(m, ddv));
+        c1 = dd_sub(c2, dd_mul_d(m, sup));
+        c2 = dd_from(0.0);
+      } else {
+        if (fabs(c0.hi) < pivmin) c0 = c0.hi < 0 ? dd_neg(pm) : pm;
+        const dd inv = dd_div(dd_from(1.0), c0);
+        u[3 * i] = inv;
+        u[3 * i + 1] = c1;
+        u[3 * i + 2] = c2;
+        x[i] = xi;
+        const dd m = dd_mul_d(inv, sub);
+        xi = dd_sub(xn, dd_mul(m, xi));
+        c0 = dd_sub(ddv, dd_mul(m, c1));
+        c1 = dd_sub(dd_from(sup), dd_mul(m, c2));
+        c2 = dd_from(0.0);
+      }
+    }
+    if (fabs(c0.hi) < pivmin) c0 = c0.hi < 0 ? dd_neg(pm) : pm;
+    // back substitution
+    dd xl = dd_div(xi, c0);
+    x[n - 1] = xl;
+    dd nrm = dd_mul(xl, xl);
+    dd xl1 = xl;  // x[i+1]
+    dd xl2 = dd_from(0.0);  // x[i+2]
+    {
+      const int64_t i = n - 2;
+      const dd v = dd_mul(dd_sub(x[i], dd_mul(u[3 * i + 1], xl1)), u[3 * i]);
+      x[i] = v;
+      nrm = dd_add(nrm, dd_mul(v, v));
+      xl2 = xl1;
+      xl1 = v;
+    }
+    for (int64_t i = n - 2; i-- > 0;) {
+      const dd r = dd_sub(dd_sub(x[i], dd_mul(u[3 * i + 1], xl1)), dd_mul(u[3 * i + 2], xl2));
+      const dd v = dd_mul(r, u[3 * i]);
+      x[i] = v;
+      nrm = dd_add(nrm, dd_mul(v, v));
+      xl2 = xl1;
+      xl1 = v;
+    }
+    final_norm = sqrt(nrm.hi);
+    // scale = 1/sqrt(nrm) in dd (one Newton step on the fp64 estimate)
+    const double s0 = 1.0 / final_norm;
+    const dd s0d = dd_from(s0);
+    const dd resid = dd_sub(dd_from(1.0), dd_mul(nrm, dd_mul(s0d, s0d)));
+    scale = dd_add(s0d, dd_mul_d(dd_mul_d(resid, s0), 0.5));
+  }
+  norms[2 * j] = scale.hi;
+  norms[2 * j + 1] = scale.lo;
+}
+
+// out[j][i] = x_j[i] * scale_j  (dd -> fp64)
+__global__ void dd_finalize_kernel(const dd* __restrict__ xs, const double* __restrict__ scales,
+                                   int64_t n, int k, double* __restrict__ out) {
+  const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (g >= n * k) return;
+  const int64_t j = g / n;
+  const dd s = {scales[2 * j], scales[2 * j + 1]};
+  const dd v = dd_mul(xs[g], s);
+  out[g] = v.hi + v.lo;
+}
+
+// canonical_sign (eig.cpp:281-289): first index of max |v| made positive.
+struct AbsMax {
+  double v;
+  int64_t i;
+};
+__device__ inline AbsMax absmax_merge(AbsMax a, AbsMax b) {
+  if (b.v > a.v || (b.v == a.v && b.i < a.i)) return b;
+  return a;
+}
+
+__global__ void absmax_kernel(const double* __restrict__ v, int64_t n, double* __restrict__ sign_out) {
+  const int j = blockIdx.x;
+  const double* row = v + static_cast<int64_t>(j) * n;
+  AbsMax best = {-1.0, 0};
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) best = absmax_merge(best, AbsMax{fabs(row[i]), i});
+  __shared__ double sv[1024];
+  __shared__ int64_t si[1024];
+  sv[threadIdx.x] = best.v;
+  si[threadIdx.x] = best.i;
+  __syncthreads();
+  for (int off = blockDim.x / 2; off > 0; off >>= 1) {
+    if (threadIdx.x < off) {
+      const AbsMax r = absmax_merge(AbsMax{sv[threadIdx.x], si[threadIdx.x]},
+                                    AbsMax{sv[threadIdx.x + off], si[threadIdx.x + off]});
+      sv[threadIdx.x] = r.v;
+      si[threadIdx.x] = r.i;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) sign_out[j] = row[si[0]] < 0.0 ? -1.0 : 1.0;
+}
+
+__global__ void scale_rows_kernel(double* __restrict__ v, int64_t n, int k, const double* __restrict__ s) {
+  const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (g >= n * k) return;
+  v[g] *= s[g / n];
+}
+
+__global__ void dpss_matrix_kernel(int64_t n, double c, double* __restrict__ diag, double* __restrict__ off) {
+  const int64_t m = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (m >= n) return;
+  // tapers.cpp:46-52, exact operation order (no contraction)
+  const double half = __dmul_rn(__dsub_rn(__dsub_rn(static_cast<double>(n), 1.0), __dmul_rn(2.0, static_cast<double>(m))), 0.5);
+  diag[m] = __dmul_rn(__dmul_rn(half, half), c);
+  if (m >= 1) off[m - 1] = __dmul_rn(static_cast<double>(m), static_cast<double>(n - m)) / 2.0;
+}
+
+// ---------------------------------------------------------------- spline
+
+constexpr double kR = -0.26794919243112270;   // sqrt(3) - 2, root of r^2 + 4r + 1
+constexpr double kC = 0.28867513459481287;    // 1/sqrt(12)
+constexpr int kFilterHalf = 36;               // |r|^36 < 3e-21
+
+// g_j = 6 (y_{j+1} - 2 y_j + y_{j-1}) / h^2 for interior j in [2, n-3]
+__device__ inline double ipow_r(int64_t e) {
+  double v = 1.0;
+  for (int64_t q = 0; q < e && q < 200; ++q) v *= kR;
+  return e > 200 ? 0.0 : v;
+}
+
+__device__ inline double moment_rhs(const double* y, int64_t j, double inv_h2) {
+  return 6.0 * (((y[j + 1] - y[j]) - (y[j] - y[j - 1])) * inv_h2);
+}
+
+__device__ inline double filter_at(const double* y, int64_t n, int64_t i, double inv_h2) {
+  const int64_t a = imax64(2, i - kFilterHalf), b = imin64(n - 3, i + kFilterHalf);
+  double left = 0.0, right = 0.0, pw = 1.0;
+  for (int64_t j = imin64(i, b); j >= a; --j) {  // sum_{j<=i} r^{i-j} g_j
+    if (j == imin64(i, b)) pw = ipow_r(i - j);
+    left = fma(pw, moment_rhs(y, j, inv_h2), left);
+    pw *= kR;
+  }
+  pw = 1.0;
+  for (int64_t j = imax64(i + 1, a); j <= b; ++j) {  // sum_{j>i} r^{j-i} g_j
+    if (j == imax64(i + 1, a)) pw = ipow_r(j - i);
+    right = fma(pw, moment_rhs(y, j, inv_h2), right);
+    pw *= kR;
+  }
+  return kC * (left + right);
+}
+
+// Second derivatives M for K rows of knot values (uniform spacing h), n >= 2*kFilterHalf+8.
+// Interior: M_{i-1} + 4 M_i + M_{i+1} = g_i (i in [2,n-3]) with the not-a-knot rows
+// giving M_1 = (y_2-2y_1+y_0)/h^2 and M_{n-2} likewise (eig.cpp:696-709 with h_i = h).
+__global__ void spline_moments_kernel(const double* __restrict__ yk, int64_t n, double h,
+                                      double* __restrict__ m_out) {
+  const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int k = blockIdx.y;
+  if (g >= n) return;
+  const double* y = yk + static_cast<int64_t>(k) * n;
+  double* M = m_out + static_cast<int64_t>(k) * n;
+  const double inv_h2 = 1.0 / (h * h);
+  const double A = ((y[2] - y[1]) - (y[1] - y[0])) * inv_h2;
+  const double B = ((y[n - 1] - y[n - 2]) - (y[n - 2] - y[n - 3])) * inv_h2;
+  auto interior = [&](int64_t i) {
+    double v = filter_at(y, n, i, inv_h2);
+    if (i - 1 < 2 * kFilterHalf) v += (A - filter_at(y, n, 1, inv_h2)) * ipow_r(i - 1);
+    if (n - 2 - i < 2 * kFilterHalf)
+      v += (B - filter_at(y, n, n - 2, inv_h2)) * ipow_r(n - 2 - i);
+    return v;
+  };
+  double v;
+  if (g == 1) v = A;
+  else if (g == n - 2) v = B;
+  else if (g == 0) v = 2.0 * A - interior(2);
+  else if (g == n - 1) v = 2.0 * B - interior(n - 3);
+  else v = interior(g);
+  M[g] = v;
+}
+
+// Small-n path: the reference's Thomas solve (eig.cpp:681-724) on one thread per row.
+__global__ void spline_moments_thomas_kernel(const double* __restrict__ xk, const double* __restrict__ yk,
+                                             int64_t n, double* __restrict__ m_out,
+                                             double* __restrict__ scratch) {
+  const int k = blockIdx.x;
+  const double* y = yk + static_cast<int64_t>(k) * n;
+  double* M = m_out + static_cast<int64_t>(k) * n;
+  const int64_t m = n - 2;
+  double* sub = scratch + static_cast<int64_t>(k) * 4 * n;
+  double* dia = sub + n;
+  double* sup = dia + n;
+  double* rhs = sup + n;
+  auto hh = [&](int64_t i) { return xk[i + 1] - xk[i]; };
+  for (int64_t i = 1; i + 1 < n; ++i) {
+    const int64_t r = i - 1;
+    sub[r] = hh(i - 1) / 6.0;
+    dia[r] = (hh(i - 1) + hh(i)) / 3.0;
+    sup[r] = hh(i) / 6.0;
+    rhs[r] = (y[i + 1] - y[i]) / hh(i) - (y[i] - y[i - 1]) / hh(i - 1);
+  }
+  {
+    const double r01 = hh(0) / hh(1);
+    dia[0] += sub[0] * (1.0 + r01);
+    sup[0] -= sub[0] * r01;
+    sub[0] = 0.0;
+  }
+  {
+    const double rr = hh(n - 2) / hh(n - 3);
+    dia[m - 1] += sup[m - 1] * (1.0 + rr);
+    sub[m - 1] -= sup[m - 1] * rr;
+    sup[m - 1] = 0.0;
+  }
+  for (int64_t r = 1; r < m; ++r) {
+    const double w = sub[r] / dia[r - 1];
+    dia[r] -= w * sup[r - 1];
+    rhs[r] -= w * rhs[r - 1];
+  }
+  M[m] = rhs[m - 1] / dia[m - 1];
+  for (int64_t r = m - 1; r-- > 0;) M[r + 1] = (rhs[r] - sup[r] * M[r + 2]) / dia[r];
+  M[0] = M[1] * (1.0 + hh(0) / hh(1)) - M[2] * (hh(0) / hh(1));
+  M[n - 1] = M[n - 2] * (1.0 + hh(n - 2) / hh(n - 3)) - M[n - 3] * (hh(n - 2) / hh(n - 3));
+}
+
+__device__ inline double knot_at(double t0, double h, int64_t i) {
+  return __dadd_rn(t0, __dmul_rn(h, static_cast<double>(i)));  // tapers.cpp:165
+}
+
+// Evaluate K splines (knots t0 + h i) at every sample time (eig.cpp:727-745).
+__global__ void spline_eval_kernel(const double* __restrict__ t, int64_t n, double t0, double h,
+                                   const double* __restrict__ yk, const double* __restrict__ mk,
+                                   int k, double* __restrict__ w) {
+  const int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (s >= n) return;
+  const double x_last = knot_at(t0, h, n - 1);
+  double xc = t[s];
+  xc = fmin(fmax(xc, t0), x_last);
+  int64_t i = static_cast<int64_t>(floor((xc - t0) / h));
+  i = imax64(0, imin64(i, n - 1));
+  // upper_bound(knots, xc) - 1 on the rounded knots
+  while (i + 1 < n && knot_at(t0, h, i + 1) <= xc) ++i;
+  while (i > 0 && knot_at(t0, h, i) > xc) --i;
+  if (i + 1 >= n) i = n - 2;
+  const double xi = knot_at(t0, h, i), xi1 = knot_at(t0, h, i + 1);
+  const double hl = xi1 - xi;
+  const double a = (xi1 - xc) / hl;
+  const double b = (xc - xi) / hl;
+  const double ca = a * a * a - a, cb = b * b * b - b, h26 = (hl * hl) / 6.0;
+  for (int kk = 0; kk < k; ++kk) {
+    const double* y = yk + static_cast<int64_t>(kk) * n;
+    const double* M = mk + static_cast<int64_t>(kk) * n;
+    w[static_cast<int64_t>(kk) * n + s] = a * y[i] + b * y[i + 1] + (ca * M[i] + cb * M[i + 1]) * h26;
+  }
+}
+
+// ---------------------------------------------------------------- R(B) quadratic form
+
+// sin / cos of 2 pi F t with the product F t reduced exactly (two-product + rint).
+__global__ void band_phase_kernel(const double* __restrict__ t, int64_t n, double f,
+                                  double* __restrict__ sn, double* __restrict__ cs) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const double p = f * t[i];
+  const double e = fma(f, t[i], -p);
+  const double r = (p - rint(p)) + e;
+  double s, c;
+  sincospi(2.0 * r, &s, &c);
+  sn[i] = s;
+  cs[i] = c;
+}
+
+constexpr int kQfRows = 256;
+constexpr int kQfCols = 256;
+constexpr int kQfChunks = 8;  // column chunks per CTA
+constexpr int kQfGroup = 8;   // weight rows per launch (register accumulators)
+
+// q_k partial over rows [row0,row1): sum_n (2F w_n^2 + 2 sum_{m>n} w_n R_nm w_m),
+// the symmetric split of sum_n w_n (R(B) w)_n (kernels.cpp:28-37).
+__global__ void __launch_bounds__(kQfRows) quadform_kernel(
+    const double* __restrict__ t, const double* __restrict__ sn, const double* __restrict__ cs,
+    const double* __restrict__ w, int64_t n, int k, double f, double tol, int64_t row0,
+    int64_t row1, double* __restrict__ partial) {
+  __shared__ double s_t[kQfCols], s_s[kQfCols], s_c[kQfCols];
+  __shared__ double s_w[kQfGroup][kQfCols];
+  const int64_t rblock = blockIdx.y;
+  const int64_t r = row0 + rblock * kQfRows + threadIdx.x;
+  const bool has_row = r < row1;
+  const int64_t col_start = static_cast<int64_t>(blockIdx.x) * kQfCols * kQfChunks;
+  const int64_t row_first = row0 + rblock * kQfRows;
+  double acc[kQfGroup];
+#pragma unroll
+  for (int kk = 0; kk < kQfGroup; ++kk) acc[kk] = 0.0;
+  const double tn = has_row ? t[r] : 0.0;
+  const double snn = has_row ? sn[r] : 0.0, csn = has_row ? cs[r] : 0.0;
+  const double two_pi_f = 2.0 * kPi * f;
+  if (col_start + kQfCols * kQfChunks - 1 >= row_first) {
+    for (int ch = 0; ch < kQfChunks; ++ch) {
+      const int64_t c0 = col_start + static_cast<int64_t>(ch) * kQfCols;
+      if (c0 >= n) break;
+      if (c0 + kQfCols - 1 < row_first) continue;
+      __syncthreads();
+      {
+        const int64_t cidx = c0 + threadIdx.x;
+        const bool ok = cidx < n;
+        s_t[threadIdx.x] = ok ? t[cidx] : 0.0;
+        s_s[threadIdx.x] = ok ? sn[cidx] : 0.0;
+        s_c[threadIdx.x] = ok ? cs[cidx] : 0.0;
+#pragma unroll
+        for (int kk = 0; kk < kQfGroup; ++kk)
+          s_w[kk][threadIdx.x] = (ok && kk < k) ? w[kk * n + cidx] : 0.0;
+      }
+      __syncthreads();
+      if (!has_row || c0 + kQfCols - 1 < r) continue;
+      const int cend = static_cast<int>(imin64(kQfCols, n - c0));
+      const int cbeg = static_cast<int>(imax64(0, r - c0));
+      for (int cc = cbeg; cc < cend; ++cc) {
+        const int64_t m = c0 + cc;
+        double v;
+        if (m == r) {
+          v = 2.0 * f;  // diagonal, counted once (kernels.cpp:108)
+        } else {
+          const double dlt = tn - s_t[cc];
+          const double adl = fabs(dlt);
+          if (adl < tol) {
+            v = 4.0 * f;  // zero-lag rule (kernels.cpp:17), pair counted twice
+          } else if (adl * f < 8.0) {
+            v = 2.0 * (sin(two_pi_f * dlt) / (kPi * dlt));  // kernels.cpp:18, near lags
+          } else {
+            v = 2.0 * ((snn * s_c[cc] - csn * s_s[cc]) / (kPi * dlt));
+          }
+        }
+#pragma unroll
+        for (int kk = 0; kk < kQfGroup; ++kk) acc[kk] = fma(v, s_w[kk][cc], acc[kk]);
+      }
+    }
+  }
+  // acc_k * w_k(n) summed over the block's rows
+  __shared__ double red[kQfRows / 32][kQfGroup];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t cta = static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x;
+#pragma unroll
+  for (int kk = 0; kk < kQfGroup; ++kk) {
+    double v = (has_row && kk < k) ? acc[kk] * w[kk * n + r] : 0.0;
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+    if (lane == 0) red[wid][kk] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < k) {
+    double sum = 0.0;
+    for (int q = 0; q < kQfRows / 32; ++q) sum += red[q][threadIdx.x];
+    partial[cta * k + threadIdx.x] = sum;
+  }
+}
+
+__global__ void reduce_partials_kernel(const double* __restrict__ partial, int64_t count, int k,
+                                       double* __restrict__ out) {
+  const int kk = blockIdx.x;
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < count; i += blockDim.x) s += partial[i * k + kk];
+  __shared__ double red[1024];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int off = blockDim.x / 2; off > 0; off >>= 1) {
+    if (threadIdx.x < off) red[threadIdx.x] += red[threadIdx.x + off];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[kk] = red[0];
+}
+
+// ---------------------------------------------------------------- concentrations
+
+__global__ void sinc_symbol_kernel(int64_t n, int64_t L, double wband, double2* __restrict__ a) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= L) return;
+  double v = 0.0;
+  int64_t lag = i <= L / 2 ? i : i - L;
+  if (lag == 0) v = 2.0 * wband;
+  else if (lag < n && lag > -n) {
+    const double lg = static_cast<double>(lag);
+    v = sin(2.0 * kPi * wband * lg) / (kPi * lg);  // tapers.cpp:71-72
+  }
+  a[i] = double2{v, 0.0};
+}
+
+__global__ void embed_kernel(const double* __restrict__ v, int64_t n, int64_t L, int k,
+                             double2* __restrict__ b) {
+  const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (g >= L * k) return;
+  const int64_t j = g / L, i = g - j * L;
+  b[g] = double2{i < n ? v[j * n + i] : 0.0, 0.0};
+}
+
+__global__ void cmul_kernel(double2* __restrict__ b, const double2* __restrict__ a, int64_t L, int k) {
+  const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (g >= L * k) return;
+  const double2 x = b[g], y = a[g % L];
+  b[g] = double2{x.x * y.x - x.y * y.y, x.x * y.y + x.y * y.x};
+}
+
+__global__ void conc_dot_kernel(const double* __restrict__ v, const double2* __restrict__ conv,
+                                int64_t n, int64_t L, double* __restrict__ out) {
+  const int j = blockIdx.x;
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += v[j * n + i] * conv[j * L + i].x;
+  __shared__ double red[256];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int off = blockDim.x / 2; off > 0; off >>= 1) {
+    if (threadIdx.x < off) red[threadIdx.x] += red[threadIdx.x + off];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[j] = red[0] / static_cast<double>(L);
+}
+
+unsigned blocks_for(int64_t n, int threads) { return static_cast<unsigned>((n + threads - 1) / threads); }
+
+double host_ms_since(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- tridiagonal top-K
+
+DpssResult tridiag_top_device(const double* d_diag, const double* d_off, int64_t n, int64_t k,
+                              double* d_vec, cudaStream_t s) {
+  require(k >= 1 && k <= n, "tridiagonal_eigen: k_top out of range");
+  // Gershgorin bounds and ||T||_inf from host copies (O(n) validation work)
+  std::vector<double> hd(n), he(n > 1 ? n - 1 : 0);
+  NUS_CUDA(cudaMemcpyAsync(hd.data(), d_diag, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (n > 1) NUS_CUDA(cudaMemcpyAsync(he.data(), d_off, (n - 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
+  NUS_CUDA(cudaStreamSynchronize(s));
+  double glo = 0, ghi = 0, anorm = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    require(std::isfinite(hd[i]) && (i + 1 >= n || std::isfinite(he[i])), "tridiagonal: non-finite input");
+    double rad = 0;
+    if (i > 0) rad += std::fabs(he[i - 1]);
+    if (i + 1 < n) rad += std::fabs(he[i]);
+    glo = i == 0 ? hd[i] - rad : std::min(glo, hd[i] - rad);
+    ghi = i == 0 ? hd[i] + rad : std::max(ghi, hd[i] + rad);
+    anorm = std::max(anorm, std::fabs(hd[i]) + rad);
+  }
+  anorm = std::max(anorm, DBL_MIN);
+  const double pad = anorm * 1e-12 + 1e-300;
+  glo -= pad;
+  ghi += pad;
+
+  DeviceBuffer e2(std::max<int64_t>(n - 1, 1) * sizeof(double));
+  if (n > 1) {
+    square_kernel<<<blocks_for(n - 1, 256), 256, 0, s>>>(d_off, n - 1, e2.as<double>());
+    note_launch();
+  }
+  // multisection: probes_per_eig probes per eigenvalue per pass
+  const int probes = 1024;
+  std::vector<double> lo(k, glo), hi(k, ghi);
+  DeviceBuffer d_lo(k * sizeof(double)), d_hi(k * sizeof(double)), d_cnt(k * probes * sizeof(int32_t));
+  std::vector<int32_t> cnt(k * probes);
+  const double pivmin = anorm * DBL_EPSILON * 1e-3;
+  const double target = 16.0 * DBL_EPSILON * anorm;
+  for (int pass = 0; pass < 16; ++pass) {
+    bool done = true;
+    for (int64_t j = 0; j < k; ++j) done = done && (hi[j] - lo[j] <= target);
+    if (done) break;
+    NUS_CUDA(cudaMemcpyAsync(d_lo.ptr, lo.data(), k * sizeof(double), cudaMemcpyHostToDevice, s));
+    NUS_CUDA(cudaMemcpyAsync(d_hi.ptr, hi.data(), k * sizeof(double), cudaMemcpyHostToDevice, s));
+    const dim3 grid(blocks_for(probes / kProbes, kSturmThreads), static_cast<unsigned>(k));
+    sturm_multisect_kernel<<<grid, kSturmThreads, 0, s>>>(d_diag, e2.as<double>(), n, d_lo.as<double>(),
+                                                          d_hi.as<double>(), probes, pivmin,
+                                                          d_cnt.as<int32_t>());
+    note_launch();
+    check_launch("sturm_multisect_kernel");
+    NUS_CUDA(cudaMemcpyAsync(cnt.data(), d_cnt.ptr, k * probes * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    NUS_CUDA(cudaStreamSynchronize(s));
+    for (int64_t j = 0; j < k; ++j) {
+      const int64_t idx = n - 1 - j;  // ascending index of the j-th largest eigenvalue
+      const double a = lo[j], b = hi[j];
+      const double step = (b - a) / static_cast<double>(probes + 1);
+      double nlo = a, nhi = b;
+      for (int p = 0; p < probes; ++p) {
+        const double lam = a + step * static_cast<double>(p + 1);
+        if (cnt[j * probes + p] > idx) { nhi = lam; break; }
+        nlo = lam;
+      }
+      if (!(nhi - nlo < b - a)) { nlo = a; nhi = b; }
+      lo[j] = nlo;
+      hi[j] = nhi;
+    }
+  }
+  DpssResult res;
+  res.values.resize(k);
+  std::vector<double> sig_hi(k), sig_lo(k);
+  for (int64_t j = 0; j < k; ++j) {
+    const double mid = 0.5 * (lo[j] + hi[j]);
+    res.values[j] = mid;
+    sig_hi[j] = mid;
+    sig_lo[j] = 0.0;
+  }
+  // inverse iteration in double-double, one thread per vector
+  DeviceBuffer d_sh(k * sizeof(double)), d_sl(k * sizeof(double)), d_norm(2 * k * sizeof(double));
+  DeviceBuffer xs(static_cast<size_t>(k) * n * sizeof(dd)), us(static_cast<size_t>(k) * n * 3 * sizeof(dd));
+  NUS_CUDA(cudaMemcpyAsync(d_sh.ptr, sig_hi.data(), k * sizeof(double), cudaMemcpyHostToDevice, s));
+  NUS_CUDA(cudaMemcpyAsync(d_sl.ptr, sig_lo.data(), k * sizeof(double), cudaMemcpyHostToDevice, s));
+  inverse_iteration_dd_kernel<<<static_cast<unsigned>(k), 1, 0, s>>>(
+      d_diag, d_off, n, d_sh.as<double>(), d_sl.as<double>(), 4, pivmin, xs.as<dd>(), us.as<dd>(),
+      d_norm.as<double>());
+  note_launch();
+  check_launch("inverse_iteration_dd_kernel");
+  dd_finalize_kernel<<<blocks_for(n * k, 256), 256, 0, s>>>(xs.as<dd>(), d_norm.as<double>(), n,
+                                                            static_cast<int>(k), d_vec);
+  note_launch();
+  DeviceBuffer sg(k * sizeof(double));
+  absmax_kernel<<<static_cast<unsigned>(k), 1024, 0, s>>>(d_vec, n, sg.as<double>());
+  note_launch();
+  scale_rows_kernel<<<blocks_for(n * k, 256), 256, 0, s>>>(d_vec, n, static_cast<int>(k), sg.as<double>());
+  note_launch();
+  check_launch("dpss finalize");
+  NUS_CUDA(cudaStreamSynchronize(s));
+  return res;
+}
+
+DpssResult dpss_device(int64_t n, double tw, int64_t k, double* d_vec, cudaStream_t s) {
+  // tapers.cpp:33-39 validation
+  require(n >= 2, "dpss_uniform: n must be >= 2");
+  require(k >= 1 && k <= n, "dpss_uniform: k_tapers out of range");
+  require(tw > 0.0 && tw < static_cast<double>(n) / 2.0, "dpss_uniform: need 0 < TW < n/2");
+  const double w = tw / static_cast<double>(n);
+  const double c = std::cos(2.0 * kPi * w);
+  DeviceBuffer diag(n * sizeof(double)), off(std::max<int64_t>(n - 1, 1) * sizeof(double));
+  dpss_matrix_kernel<<<blocks_for(n, 256), 256, 0, s>>>(n, c, diag.as<double>(), off.as<double>());
+  note_launch();
+  check_launch("dpss_matrix_kernel");
+  return tridiag_top_device(diag.as<double>(), off.as<double>(), n, k, d_vec, s);
+}
+
+void dpss_concentrations(int64_t n, double tw, int64_t k, const double* d_vec, double* conc,
+                         cudaStream_t s) {
+  const double wband = tw / static_cast<double>(n);
+  int64_t L = 1;
+  while (L < 2 * n) L <<= 1;
+  DeviceBuffer a(L * sizeof(double2)), b(static_cast<size_t>(L) * k * sizeof(double2)), out(k * sizeof(double));
+  sinc_symbol_kernel<<<blocks_for(L, 256), 256, 0, s>>>(n, L, wband, a.as<double2>());
+  embed_kernel<<<blocks_for(L * k, 256), 256, 0, s>>>(d_vec, n, L, static_cast<int>(k), b.as<double2>());
+  note_launch(2);
+  cufftHandle h1, hk;
+  NUS_CUFFT(cufftPlan1d(&h1, static_cast<int>(L), CUFFT_Z2Z, 1));
+  NUS_CUFFT(cufftPlan1d(&hk, static_cast<int>(L), CUFFT_Z2Z, static_cast<int>(k)));
+  NUS_CUFFT(cufftSetStream(h1, s));
+  NUS_CUFFT(cufftSetStream(hk, s));
+  NUS_CUFFT(cufftExecZ2Z(h1, a.as<cufftDoubleComplex>(), a.as<cufftDoubleComplex>(), CUFFT_FORWARD));
+  NUS_CUFFT(cufftExecZ2Z(hk, b.as<cufftDoubleComplex>(), b.as<cufftDoubleComplex>(), CUFFT_FORWARD));
+  cmul_kernel<<<blocks_for(L * k, 256), 256, 0, s>>>(b.as<double2>(), a.as<double2>(), L, static_cast<int>(k));
+  note_launch();
+  NUS_CUFFT(cufftExecZ2Z(hk, b.as<cufftDoubleComplex>(), b.as<cufftDoubleComplex>(), CUFFT_INVERSE));
+  conc_dot_kernel<<<static_cast<unsigned>(k), 256, 0, s>>>(d_vec, b.as<double2>(), n, L, out.as<double>());
+  note_launch();
+  check_launch("dpss_concentrations");
+  NUS_CUDA(cudaMemcpyAsync(conc, out.ptr, k * sizeof(double), cudaMemcpyDeviceToHost, s));
+  NUS_CUDA(cudaStreamSynchronize(s));
+  cufftDestroy(h1);
+  cufftDestroy(hk);
+  for (int64_t j = 0; j < k; ++j) conc[j] = std::min(std::max(conc[j], 0.0), 1.0);  // tapers.cpp:76
+}
+
+void spline_uniform_device(const double* d_t, int64_t n, const double* d_y, int64_t k,
+                           double* d_w, cudaStream_t s) {
+  require(n >= 4, "CubicSpline: need at least 4 knots");
+  double t0 = 0, tl = 0;
+  NUS_CUDA(cudaMemcpyAsync(&t0, d_t, sizeof(double), cudaMemcpyDeviceToHost, s));
+  NUS_CUDA(cudaMemcpyAsync(&tl, d_t + n - 1, sizeof(double), cudaMemcpyDeviceToHost, s));
+  NUS_CUDA(cudaStreamSynchronize(s));
+  const double h = (tl - t0) / static_cast<double>(n - 1);  // tapers.cpp:156
+  DeviceBuffer moments(static_cast<size_t>(k) * n * sizeof(double));
+  if (n >= 4 * kFilterHalf + 16) {
+    const dim3 grid(blocks_for(n, 256), static_cast<unsigned>(k));
+    spline_moments_kernel<<<grid, 256, 0, s>>>(d_y, n, h, moments.as<double>());
+    note_launch();
+  } else {
+    DeviceBuffer knots(n * sizeof(double)), scratch(static_cast<size_t>(k) * 4 * n * sizeof(double));
+    std::vector<double> hk(n);
+    for (int64_t i = 0; i < n; ++i) hk[i] = t0 + h * static_cast<double>(i);
+    NUS_CUDA(cudaMemcpyAsync(knots.ptr, hk.data(), n * sizeof(double), cudaMemcpyHostToDevice, s));
+    spline_moments_thomas_kernel<<<static_cast<unsigned>(k), 1, 0, s>>>(knots.as<double>(), d_y, n,
+                                                                        moments.as<double>(),
+                                                                        scratch.as<double>());
+    note_launch();
+    NUS_CUDA(cudaStreamSynchronize(s));
+  }
+  check_launch("spline moments");
+  spline_eval_kernel<<<blocks_for(n, 256), 256, 0, s>>>(d_t, n, t0, h, d_y, moments.as<double>(),
+                                                        static_cast<int>(k), d_w);
+  note_launch();
+  check_launch("spline_eval_kernel");
+  NUS_CUDA(cudaStreamSynchronize(s));
+}
+
+void quadform_device(const double* d_t, int64_t n, double f_max, const double* d_w, int64_t k,
+                     int64_t row0, int64_t row1, double* q_host, cudaStream_t s) {
+  require(k >= 1 && k <= kQfGroup, "quadratic_form: at most 8 weight rows per launch");
+  require(row0 >= 0 && row1 <= n && row0 <= row1, "quadratic_form: bad row range");
+  if (row0 == row1) {
+    for (int64_t j = 0; j < k; ++j) q_host[j] = 0.0;
+    return;
+  }
+  double t0 = 0, tl = 0;
+  NUS_CUDA(cudaMemcpyAsync(&t0, d_t, sizeof(double), cudaMemcpyDeviceToHost, s));
+  NUS_CUDA(cudaMemcpyAsync(&tl, d_t + n - 1, sizeof(double), cudaMemcpyDeviceToHost, s));
+  NUS_CUDA(cudaStreamSynchronize(s));
+  const double mean_dt = (tl - t0) / static_cast<double>(n);  // grid.cpp:21
+  const double tol = 1e-12 * mean_dt;                          // kernels.cpp:103
+  DeviceBuffer sn(n * sizeof(double)), cs(n * sizeof(double));
+  band_phase_kernel<<<blocks_for(n, 256), 256, 0, s>>>(d_t, n, f_max, sn.as<double>(), cs.as<double>());
+  note_launch();
+  const int64_t rblocks = (row1 - row0 + kQfRows - 1) / kQfRows;
+  const int64_t cgroups = (n + kQfCols * kQfChunks - 1) / (kQfCols * kQfChunks);
+  require(rblocks < 65536, "quadratic_form: too many row blocks for one launch");
+  const dim3 grid(static_cast<unsigned>(cgroups), static_cast<unsigned>(rblocks));
+  const int64_t ncta = cgroups * rblocks;
+  DeviceBuffer partial(static_cast<size_t>(ncta) * k * sizeof(double)), out(k * sizeof(double));
+  quadform_kernel<<<grid, kQfRows, 0, s>>>(d_t, sn.as<double>(), cs.as<double>(), d_w, n,
+                                           static_cast<int>(k), f_max, tol, row0, row1,
+                                           partial.as<double>());
+  note_launch();
+  check_launch("quadform_kernel");
+  reduce_partials_kernel<<<static_cast<unsigned>(k), 1024, 0, s>>>(partial.as<double>(), ncta,
+                                                                   static_cast<int>(k), out.as<double>());
+  note_launch();
+  check_launch("reduce_partials_kernel");
+  NUS_CUDA(cudaMemcpyAsync(q_host, out.ptr, k * sizeof(double), cudaMemcpyDeviceToHost, s));
+  NUS_CUDA(cudaStreamSynchronize(s));
+}
+
+namespace {
+__global__ void scale_by_kernel(double* __restrict__ w, int64_t n, int k, const double* __restrict__ s) {
+  const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (g >= n * k) return;
+  w[g] *= s[g / n];
+}
+}  // namespace
+
+void gpss_interpolated_device(const double* d_t, const double* h_t, int64_t n, double f_max,
+                              double f_w, int64_t k, double* d_w, cudaStream_t s, double* ms_dpss,
+                              double* ms_spline, double* ms_norm) {
+  // tapers.cpp:146-160 validation, same order and exception types
+  require(n >= 8, "gpss_interpolated: need at least 8 samples");
+  require(f_w > 0.0, "gpss_interpolated: f_w must be positive");
+  require(std::isfinite(f_w), "AnalysisBand: half_width must be positive");
+  require(f_max > 0.0 && std::isfinite(f_max), "SignalBand: f_max must be positive");
+  if (!(f_w <= f_max + 1e-12 * f_max))
+    fail(NUS_ERR_BAND_RANGE, "gpss_interpolated: nominal band not inside signal band");
+  const double h = (h_t[n - 1] - h_t[0]) / static_cast<double>(n - 1);
+  const double tw = f_w * h * static_cast<double>(n);
+  require(tw < static_cast<double>(n) / 2.0, "gpss_interpolated: f_w too large for this grid");
+  auto t0 = std::chrono::steady_clock::now();
+  DeviceBuffer dp(static_cast<size_t>(k) * n * sizeof(double));
+  dpss_device(n, tw, k, dp.as<double>(), s);
+  if (ms_dpss) *ms_dpss = host_ms_since(t0);
+  t0 = std::chrono::steady_clock::now();
+  spline_uniform_device(d_t, n, dp.as<double>(), k, d_w, s);
+  if (ms_spline) *ms_spline = host_ms_since(t0);
+  t0 = std::chrono::steady_clock::now();
+  std::vector<double> q(k), scale(k);
+  for (int64_t k0 = 0; k0 < k; k0 += kQfGroup) {
+    const int64_t kk = std::min<int64_t>(kQfGroup, k - k0);
+    quadform_device(d_t, n, f_max, d_w + k0 * n, kk, 0, n, q.data() + k0, s);
+  }
+  for (int64_t j = 0; j < k; ++j) {
+    if (!(q[j] > 0.0)) fail(NUS_ERR_NUMERIC, "gpss_interpolated: degenerate metric norm");
+    scale[j] = std::sqrt(2.0 * f_w / q[j]);  // tapers.cpp:177
+  }
+  DeviceBuffer ds(k * sizeof(double));
+  NUS_CUDA(cudaMemcpyAsync(ds.ptr, scale.data(), k * sizeof(double), cudaMemcpyHostToDevice, s));
+  scale_by_kernel<<<blocks_for(n * k, 256), 256, 0, s>>>(d_w, n, static_cast<int>(k), ds.as<double>());
+  note_launch();
+  check_launch("scale_by_kernel");
+  NUS_CUDA(cudaStreamSynchronize(s));
+  if (ms_norm) *ms_norm = host_ms_since(t0);
+}
+
+}  // namespace nus
