@@ -158,6 +158,11 @@ int nus_mtnufft_spread_device(nus_mtnufft_t est, const void* x_dev, int32_t x_dt
                               int64_t s1, void* grid_dev, int64_t k_pad, void* stream);
 int nus_mtnufft_transform_device(nus_mtnufft_t est, void* grid_dev, int64_t k0, int64_t k1,
                                  double divisor, int32_t accumulate, void* power_dev, void* stream);
+/* Per-stage CUDA-event timing of the fast path: record (on the caller's stream) the
+ * next max_runs estimate calls; _read syncs and returns summed ms for
+ * [spread, fft, crop+power] and the number of runs recorded. */
+int nus_mtnufft_timing(nus_mtnufft_t est, int64_t max_runs);
+int nus_mtnufft_timing_read(nus_mtnufft_t est, double* stage_ms3, int64_t* runs);
 /* Algorithmic bytes of one estimate (SURVEY §8d model) and of its spreading kernel. */
 int nus_mtnufft_bytes_model(nus_mtnufft_t est, int32_t x_dtype, double* total, double* spread,
                             double* fft, double* crop);

@@ -109,6 +109,8 @@ _SIGS = {
     "nus_mtnufft_spread_device": [_vp, _vp, _i32, _i64, _i64, _vp, _i64, _vp],
     "nus_mtnufft_transform_device": [_vp, _vp, _i64, _i64, _d, _i32, _vp, _vp],
     "nus_mtnufft_bytes_model": [_vp, _i32, _dp, _dp, _dp, _dp],
+    "nus_mtnufft_timing": [_vp, _i64],
+    "nus_mtnufft_timing_read": [_vp, _dp, _i64p],
 }
 _RESTYPE = {"nus_last_error": ctypes.c_char_p, "nus_kernel_launch_count": _i64}
 

@@ -432,6 +432,22 @@ int nus_mtnufft_transform_device(nus_mtnufft_t est, void* grid_dev, int64_t k0, 
   });
 }
 
+int nus_mtnufft_timing(nus_mtnufft_t est, int64_t max_runs) {
+  return guarded([&] {
+    nus::require(est && max_runs >= 0, "nus_mtnufft_timing: bad argument");
+    nus::use_device(est->est->cfg.device);
+    nus::estimator_timing_enable(*est->est, static_cast<size_t>(max_runs));
+  });
+}
+
+int nus_mtnufft_timing_read(nus_mtnufft_t est, double* stage_ms3, int64_t* runs) {
+  return guarded([&] {
+    nus::require(est && stage_ms3 && runs, "nus_mtnufft_timing_read: null argument");
+    nus::use_device(est->est->cfg.device);
+    nus::estimator_timing_read(*est->est, stage_ms3, runs);
+  });
+}
+
 int nus_mtnufft_bytes_model(nus_mtnufft_t est, int32_t x_dtype, double* total, double* spread,
                             double* fft, double* crop) {
   return guarded([&] {

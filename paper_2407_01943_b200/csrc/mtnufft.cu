@@ -141,8 +141,18 @@ void estimator_run(Estimator& est, const void* x_dev, int x_dtype, void* power_d
     a.k = K;
     a.kpad = K;
     a.grid = est.grid.ptr;
+    const bool timed = est.tslot < est.tcap;
+    cudaEvent_t* ev = timed ? est.tev.data() + 4 * est.tslot : nullptr;
+    if (timed) NUS_CUDA(cudaEventRecord(ev[0], s));
     launch_spread(plan, a, s);
-    run_transform(plan, est.grid.ptr, K, K, j_dev, power_dev, power_f64, static_cast<double>(K), false, s);
+    if (timed) NUS_CUDA(cudaEventRecord(ev[1], s));
+    run_fft(plan, est.grid.ptr, K, K, s);
+    if (timed) NUS_CUDA(cudaEventRecord(ev[2], s));
+    run_crop(plan, est.grid.ptr, K, K, j_dev, power_dev, power_f64, static_cast<double>(K), false, s);
+    if (timed) {
+      NUS_CUDA(cudaEventRecord(ev[3], s));
+      ++est.tslot;
+    }
     return;
   }
   // direct path: exact sums in fp64 (nufft.cpp:174-186)
@@ -208,12 +218,35 @@ void estimator_estimate_host(Estimator& est, const double* x, double* power, dou
   NUS_CUDA(cudaStreamSynchronize(s));
 }
 
+void estimator_timing_enable(Estimator& est, size_t max_runs) {
+  for (auto e : est.tev) cudaEventDestroy(e);
+  est.tev.assign(4 * max_runs, nullptr);
+  for (auto& e : est.tev) NUS_CUDA(cudaEventCreate(&e));
+  est.tslot = 0;
+  est.tcap = max_runs;
+}
+
+void estimator_timing_read(Estimator& est, double* ms3, int64_t* runs) {
+  ms3[0] = ms3[1] = ms3[2] = 0.0;
+  for (size_t r = 0; r < est.tslot; ++r) {
+    cudaEvent_t* ev = est.tev.data() + 4 * r;
+    NUS_CUDA(cudaEventSynchronize(ev[3]));
+    for (int q = 0; q < 3; ++q) {
+      float ms = 0.f;
+      NUS_CUDA(cudaEventElapsedTime(&ms, ev[q], ev[q + 1]));
+      ms3[q] += ms;
+    }
+  }
+  *runs = static_cast<int64_t>(est.tslot);
+}
+
 cudaStream_t Estimator::stream() {
   if (!own_stream) NUS_CUDA(cudaStreamCreateWithFlags(&own_stream, cudaStreamNonBlocking));
   return own_stream;
 }
 
 Estimator::~Estimator() {
+  for (auto e : tev) cudaEventDestroy(e);
   if (own_stream) cudaStreamDestroy(own_stream);
 }
 

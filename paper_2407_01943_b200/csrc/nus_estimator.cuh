@@ -15,6 +15,11 @@ struct Estimator {
   double setup_ms[5] = {0, 0, 0, 0, 0};
   std::mutex mu;
   cudaStream_t own_stream = nullptr;
+  // optional per-stage CUDA-event timing: 4 events per run (before spread,
+  // after spread, after FFT, after crop) recorded on the caller's stream
+  std::vector<cudaEvent_t> tev;
+  size_t tslot = 0;         // runs recorded
+  size_t tcap = 0;          // capacity in runs
   cudaStream_t stream();
   ~Estimator();
 };
@@ -24,6 +29,8 @@ std::unique_ptr<Estimator> estimator_create(const nus_mtnufft_config_t& cfg, con
 void estimator_run(Estimator& est, const void* x_dev, int x_dtype, void* power_dev, bool power_f64,
                    void* j_dev, cudaStream_t s);
 void estimator_estimate_host(Estimator& est, const double* x, double* power, double* j);
+void estimator_timing_enable(Estimator& est, size_t max_runs);
+void estimator_timing_read(Estimator& est, double* ms3, int64_t* runs);
 void estimator_bytes(const Estimator& est, int x_dtype, double* total, double* spread, double* fft,
                      double* crop);
 

@@ -144,6 +144,10 @@ void launch_spread(const Plan& plan, const SpreadArgs& a, cudaStream_t s);
 void run_transform(Plan& plan, void* grid, int64_t k, int64_t kpad, void* j_out, void* power,
                    bool power_f64, double divisor, bool accumulate, cudaStream_t s);
 
+void run_fft(Plan& plan, void* grid, int64_t k, int64_t kpad, cudaStream_t s);
+void run_crop(Plan& plan, void* grid, int64_t k, int64_t kpad, void* j_out, void* power,
+              bool power_f64, double divisor, bool accumulate, cudaStream_t s);
+
 void launch_ndft_direct(const double* d_t, int64_t n, const void* d_y, bool y_f32,
                         const double* d_c, int64_t nc, void* d_out, bool out_f32, int64_t batch,
                         cudaStream_t s);

@@ -44,8 +44,7 @@ __global__ void crop_power_kernel(const typename V2<Real>::T* __restrict__ grid,
 
 }  // namespace
 
-void run_transform(Plan& plan, void* grid, int64_t k, int64_t kpad, void* j_out, void* power,
-                   bool power_f64, double divisor, bool accumulate, cudaStream_t s) {
+void run_fft(Plan& plan, void* grid, int64_t k, int64_t kpad, cudaStream_t s) {
   const PlanParams& p = plan.p;
   const bool f64 = p.precision == NUS_F64;
   const size_t cbytes = f64 ? sizeof(double2) : sizeof(float2);
@@ -71,6 +70,12 @@ void run_transform(Plan& plan, void* grid, int64_t k, int64_t kpad, void* j_out,
                                reinterpret_cast<cufftComplex*>(base), CUFFT_FORWARD));
     }
   }
+}
+
+void run_crop(Plan& plan, void* grid, int64_t k, int64_t kpad, void* j_out, void* power,
+              bool power_f64, double divisor, bool accumulate, cudaStream_t s) {
+  const PlanParams& p = plan.p;
+  const bool f64 = p.precision == NUS_F64;
   const dim3 gridd(static_cast<unsigned>((p.nc + 255) / 256), static_cast<unsigned>(p.channels));
   const int acc = accumulate ? 1 : 0;
   if (f64)
@@ -90,6 +95,12 @@ void run_transform(Plan& plan, void* grid, int64_t k, int64_t kpad, void* j_out,
         divisor, acc);
   note_launch();
   check_launch("crop_power_kernel");
+}
+
+void run_transform(Plan& plan, void* grid, int64_t k, int64_t kpad, void* j_out, void* power,
+                   bool power_f64, double divisor, bool accumulate, cudaStream_t s) {
+  run_fft(plan, grid, k, kpad, s);
+  run_crop(plan, grid, k, kpad, j_out, power, power_f64, divisor, accumulate, s);
 }
 
 }  // namespace nus
