@@ -84,11 +84,11 @@ struct PlanParams {
 };
 
 struct SpreadTables {
-  int tile = 512;               // cells per spreading tile
+  int tile = 128;               // cells per spreading tile (= spread.cu kTile)
   int64_t ntiles = 0;
   DeviceBuffer start;           // int32 [C][n] start cell s = j0 mod Mr (sorted)
   DeviceBuffer perm;            // int32 [C][n] original sample index of sorted point
-  DeviceBuffer frac;            // real  [C][n] fractional cell offset in [0,1)
+  DeviceBuffer gauss;           // real2 [C][n] (A, g): W_p = A g^p C_p for the point's 2w cells
   DeviceBuffer prephase;        // real2 [C][n] e^{-i 2pi fshift t}
   DeviceBuffer tile_range;      // int32 [C][ntiles+1][2]: point range of tile (lo, hi)
   DeviceBuffer wrap_lo;         // int32 [C]: first sorted point whose support wraps into tile 0

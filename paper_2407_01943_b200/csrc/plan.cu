@@ -169,8 +169,8 @@ __global__ void sorted_tables_kernel(const double* __restrict__ t, int64_t n, in
                                      const uint64_t* __restrict__ keys_sorted,
                                      const int32_t* __restrict__ perm, int mr_bits,
                                      double neg2pi_df, double neg2pi_fshift, double mr_d,
-                                     int32_t* __restrict__ start, Real* __restrict__ frac,
-                                     Real* __restrict__ prephase) {
+                                     double beta, int w2, int32_t* __restrict__ start,
+                                     Real* __restrict__ gauss, Real* __restrict__ prephase) {
   const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (g >= total) return;
   const int64_t c = g / n;
@@ -181,7 +181,12 @@ __global__ void sorted_tables_kernel(const double* __restrict__ t, int64_t n, in
   const double fr = cell - floor(cell);
   const uint64_t mask = (static_cast<uint64_t>(1) << mr_bits) - 1;
   start[g] = static_cast<int32_t>(keys_sorted[g] & mask);
-  frac[g] = static_cast<Real>(fr);
+  // Gaussian factors around the support centre, fr' = frac - 1/2:
+  //   exp(-beta (frac + w - 1 - p)^2) = A g^p C_p,  g = e^{2 beta fr'},
+  //   A = e^{-beta fr' (fr' + 2w - 1)},  C_p = e^{-beta (p - w + 1/2)^2}
+  const double frc = fr - 0.5;
+  gauss[2 * g] = static_cast<Real>(exp(-beta * frc * (frc + static_cast<double>(w2 - 1))));
+  gauss[2 * g + 1] = static_cast<Real>(exp(2.0 * beta * frc));
   double sn, cs;
   sincos(__dmul_rn(neg2pi_fshift, tv), &sn, &cs);  // nufft.cpp:116-117
   prephase[2 * g] = static_cast<Real>(cs);
@@ -247,7 +252,7 @@ void plan_build_tables(Plan& plan, cudaStream_t st) {
   tb.first_cell.alloc(total * sizeof(int64_t));
   tb.start.alloc(total * sizeof(int32_t));
   tb.perm.alloc(total * sizeof(int32_t));
-  tb.frac.alloc(total * rs);
+  tb.gauss.alloc(total * 2 * rs);
   tb.prephase.alloc(total * 2 * rs);
 
   DeviceBuffer keys(total * sizeof(uint64_t)), keys_sorted(total * sizeof(uint64_t));
@@ -279,17 +284,17 @@ void plan_build_tables(Plan& plan, cudaStream_t st) {
   if (p.precision == NUS_F64)
     sorted_tables_kernel<double><<<blocks, threads, 0, st>>>(
         plan.d_times.as<double>(), p.n, total, keys_sorted.as<uint64_t>(), tb.perm.as<int32_t>(),
-        mr_bits, neg2pi_df, neg2pi_fshift, mr_d, tb.start.as<int32_t>(), tb.frac.as<double>(),
-        tb.prephase.as<double>());
+        mr_bits, neg2pi_df, neg2pi_fshift, mr_d, p.beta, 2 * p.w, tb.start.as<int32_t>(),
+        tb.gauss.as<double>(), tb.prephase.as<double>());
   else
     sorted_tables_kernel<float><<<blocks, threads, 0, st>>>(
         plan.d_times.as<double>(), p.n, total, keys_sorted.as<uint64_t>(), tb.perm.as<int32_t>(),
-        mr_bits, neg2pi_df, neg2pi_fshift, mr_d, tb.start.as<int32_t>(), tb.frac.as<float>(),
-        tb.prephase.as<float>());
+        mr_bits, neg2pi_df, neg2pi_fshift, mr_d, p.beta, 2 * p.w, tb.start.as<int32_t>(),
+        tb.gauss.as<float>(), tb.prephase.as<float>());
   note_launch();
   check_launch("sorted_tables_kernel");
 
-  tb.tile = static_cast<int>(std::min<int64_t>(512, p.mr));
+  tb.tile = static_cast<int>(std::min<int64_t>(128, p.mr));  // = spread.cu kTile
   require(tb.tile >= 2 * p.w, "NufftPlan: spread width exceeds the tile size");
   tb.ntiles = p.mr / tb.tile;
   tb.tile_range.alloc(p.channels * (tb.ntiles + 1) * 2 * sizeof(int32_t));

@@ -14,10 +14,13 @@
 //     z_k  = w_k(t) * x * e^{-i 2 pi fshift t}  (k < KG)
 //     W_p  = exp(-beta (d - p)^2),  p < 2w,  d = frac + w - 1
 // where W_p uses one exp pair per point (Greengard-Lee style factorisation
-// around the support centre).  Each thread then owns R consecutive cells and
-// sums the contributions of the points covering them (binary search in the
-// staged batch), accumulating K complex values per cell in registers.  Every
-// cell of the grid is written exactly once (zeros included), so no memset.
+// around the support centre).  Each WARP then owns 32 consecutive cells (one
+// per lane) and walks, in lock-step, the staged points whose support meets
+// them: the point's z_k are warp-wide shared-memory broadcasts (one
+// wavefront per 16 B) and only the Gaussian weight is a per-lane read, so
+// there is no per-lane search and no trip-count divergence.  K complex
+// accumulators per cell live in registers.  Every cell of the grid is written
+// exactly once (zeros included), so no memset.
 #include <algorithm>
 
 #include "nus_internal.cuh"
@@ -26,9 +29,9 @@ namespace nus {
 
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kCellsPerThread = 2;   // R
-constexpr int kBatch = 128;          // points staged per pass
+constexpr int kThreads = 128;
+constexpr int kTile = kThreads;      // one cell per thread, 32 per warp
+constexpr int kBatch = 128;          // points staged per pass (a C2 tile holds ~76)
 constexpr int kMaxW2 = 64;
 
 template <typename Real> struct Vec2;
@@ -39,7 +42,7 @@ template <typename Real>
 struct SpreadParams {
   const int32_t* start;
   const int32_t* perm;
-  const Real* frac;
+  const typename Vec2<Real>::T* gauss;  // per point (A, g): W_p = A g^p C_p
   const Real* prephase;
   const int32_t* ranges;
   const int32_t* wrap_lo;
@@ -52,51 +55,45 @@ struct SpreadParams {
   Real beta, cq[kMaxW2];
 };
 
-__device__ inline int lower_bound_smem(const int* a, int n, int v) {
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (a[mid] < v) lo = mid + 1; else hi = mid;
-  }
-  return lo;
-}
-
 template <typename Real, int KG>
-__global__ void __launch_bounds__(kThreads) spread_gather_kernel(const SpreadParams<Real> P) {
+__global__ void __launch_bounds__(kThreads, 5) spread_gather_kernel(const SpreadParams<Real> P) {
   using R2 = typename Vec2<Real>::T;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   R2* sm_z = reinterpret_cast<R2*>(smem_raw);                         // [kBatch][KG]
   Real* sm_w = reinterpret_cast<Real*>(sm_z + kBatch * KG);          // [kBatch][w2s]
-  const int w2s = P.w2 | 1;
+  const int w2s = P.w2 + 1;  // odd stride (w2 is even) spreads rows over banks
   int* sm_rel = reinterpret_cast<int*>(sm_w + kBatch * w2s);         // [kBatch]
 
   const int64_t tile_id = blockIdx.x;
   const int64_t c = blockIdx.y;
-  const int kg = P.kg;
   const int64_t c0 = tile_id * P.tile;
   const int64_t base = c * P.n;
-  const int r0 = threadIdx.x * kCellsPerThread;
+  const int lane = threadIdx.x & 31;
+  const int wcell = threadIdx.x & ~31;        // warp's first cell inside the tile
+  const int cell = threadIdx.x;               // this lane's cell inside the tile
+  const bool warp_live = wcell < P.tile;
 
-  R2 acc[kCellsPerThread][KG];
+  R2 acc[KG];
 #pragma unroll
-  for (int j = 0; j < kCellsPerThread; ++j)
-#pragma unroll
-    for (int k = 0; k < KG; ++k) acc[j][k] = R2{Real(0), Real(0)};
+  for (int k = 0; k < KG; ++k) acc[k] = R2{Real(0), Real(0)};
 
   const int32_t* rng = P.ranges + 2 * (c * (P.ntiles + 1) + tile_id);
   // segment 0: wrapping points (tile 0 only); segment 1: the tile's own range
-  const int seg_lo[2] = {tile_id == 0 ? P.wrap_lo[c] : 0, rng[0]};
-  const int seg_hi[2] = {tile_id == 0 ? static_cast<int>(P.n) : 0, rng[1]};
-  const int64_t seg_shift[2] = {c0 + P.mr, c0};
+  const int wrap_lo = tile_id == 0 ? P.wrap_lo[c] : 0;
+  const int wrap_hi = tile_id == 0 ? static_cast<int>(P.n) : 0;
+  const int own_lo = rng[0], own_hi = rng[1];
 
   for (int seg = 0; seg < 2; ++seg) {
-    for (int b0 = seg_lo[seg]; b0 < seg_hi[seg]; b0 += kBatch) {
-      const int nb = min(kBatch, seg_hi[seg] - b0);
+    const int lo_s = seg == 0 ? wrap_lo : own_lo;
+    const int hi_s = seg == 0 ? wrap_hi : own_hi;
+    const int64_t shift = seg == 0 ? c0 + P.mr : c0;
+    for (int b0 = lo_s; b0 < hi_s; b0 += kBatch) {
+      const int nb = min(kBatch, hi_s - b0);
       __syncthreads();
       for (int j = threadIdx.x; j < nb; j += kThreads) {
         const int64_t gi = base + b0 + j;
         const int32_t ti = P.perm[gi];
-        sm_rel[j] = static_cast<int>(static_cast<int64_t>(P.start[gi]) - seg_shift[seg]);
+        sm_rel[j] = static_cast<int>(static_cast<int64_t>(P.start[gi]) - shift);
         // sample value times prephase
         Real xr, xi;
         if (P.x_complex) {
@@ -113,67 +110,66 @@ __global__ void __launch_bounds__(kThreads) spread_gather_kernel(const SpreadPar
           xi = Real(0);
         }
         if (ti < P.s0 || ti >= P.s1) { xr = Real(0); xi = Real(0); }
-        const Real pr = P.prephase[2 * gi], pi = P.prephase[2 * gi + 1];
-        const Real yr = xr * pr - xi * pi;
-        const Real yi = xr * pi + xi * pr;
+        const R2 ph = reinterpret_cast<const R2*>(P.prephase)[gi];
+        const Real yr = xr * ph.x - xi * ph.y;
+        const Real yi = xr * ph.y + xi * ph.x;
 #pragma unroll
         for (int k = 0; k < KG; ++k) {
           Real wk = Real(1);
-          if (P.tapers != nullptr && k < kg)
-            wk = P.tapers[(c * P.k_total + P.k0 + k) * P.n + (b0 + j)];
-          if (k >= kg) wk = Real(0);
+          if (P.tapers != nullptr) wk = P.tapers[(c * P.k_total + P.k0 + k) * P.n + (b0 + j)];
           sm_z[j * KG + k] = R2{wk * yr, wk * yi};
         }
-        // Gaussian weights W_p = A g^p C_p, fr' = frac - 1/2
-        const Real fr = P.frac[gi] - Real(0.5);
-        Real gval = exp(Real(2) * P.beta * fr);
-        Real a = exp(-P.beta * fr * (fr + Real(P.w2 - 1)));
+        // Gaussian weights W_p = A g^p C_p (A, g precomputed per point at plan time);
+        // two interleaved recurrences (even / odd p) halve the dependent chain.
+        const R2 ag = P.gauss[gi];
+        const Real g2 = ag.y * ag.y;
+        Real ae = ag.x;
+        Real ao = ag.x * ag.y;
         Real* wrow = sm_w + j * w2s;
-        for (int p = 0; p < P.w2; ++p) {
-          wrow[p] = a * P.cq[p];
-          a *= gval;
+        for (int p = 0; p < P.w2; p += 2) {
+          wrow[p] = ae * P.cq[p];
+          wrow[p + 1] = ao * P.cq[p + 1];
+          ae *= g2;
+          ao *= g2;
         }
       }
       __syncthreads();
-      const int lo = lower_bound_smem(sm_rel, nb, r0 - (P.w2 - 1));
-      const int hi = lower_bound_smem(sm_rel, nb, r0 + kCellsPerThread);
+      if (!warp_live) continue;
+      // points of this batch meeting the warp's cells [wcell, wcell+32): count the staged
+      // rel values below each bound with ballots (no serial search)
+      int lo = 0, hi = 0;
+      for (int j0 = 0; j0 < nb; j0 += 32) {
+        const int j = j0 + lane;
+        const int r = j < nb ? sm_rel[j] : 0x7fffffff;
+        lo += __popc(__ballot_sync(0xffffffffu, r < wcell - (P.w2 - 1)));
+        hi += __popc(__ballot_sync(0xffffffffu, r < wcell + 32));
+      }
       for (int i = lo; i < hi; ++i) {
-        const int p0 = r0 - sm_rel[i];
-        R2 z[KG];
+        const int p = cell - sm_rel[i];            // broadcast read
+        const bool in = p >= 0 && p < P.w2;
+        const Real wt = in ? sm_w[i * w2s + (in ? p : 0)] : Real(0);
+        const R2* zr = sm_z + i * KG;
 #pragma unroll
-        for (int k = 0; k < KG; ++k) z[k] = sm_z[i * KG + k];
-        const Real* wrow = sm_w + i * w2s;
-#pragma unroll
-        for (int j = 0; j < kCellsPerThread; ++j) {
-          const int p = p0 + j;
-          if (p >= 0 && p < P.w2) {
-            const Real wt = wrow[p];
-#pragma unroll
-            for (int k = 0; k < KG; ++k) {
-              acc[j][k].x = fma(wt, z[k].x, acc[j][k].x);
-              acc[j][k].y = fma(wt, z[k].y, acc[j][k].y);
-            }
-          }
+        for (int k = 0; k < KG; ++k) {
+          const R2 z = zr[k];                      // broadcast read
+          acc[k].x = fma(wt, z.x, acc[k].x);
+          acc[k].y = fma(wt, z.y, acc[k].y);
         }
       }
     }
   }
-  // write every cell of the tile (zeros included)
-  if (r0 >= P.tile) return;
+  // write every cell of the tile (zeros included): 32 consecutive cells per warp and row
+  if (cell >= P.tile) return;
 #pragma unroll
-  for (int k = 0; k < KG; ++k) {
-    if (k < kg) {
-      R2* row = P.grid + (c * P.kpad + P.k0 + k) * P.mr + c0 + r0;
-#pragma unroll
-      for (int j = 0; j < kCellsPerThread; ++j) row[j] = acc[j][k];
-    }
-  }
+  for (int k = 0; k < KG; ++k)
+    P.grid[(c * P.kpad + P.k0 + k) * P.mr + c0 + cell] = acc[k];
+  (void)lane;
 }
 
 template <typename Real, int KG>
 void launch_group(const SpreadParams<Real>& P, int64_t channels, cudaStream_t s) {
   const size_t smem = kBatch * KG * sizeof(typename Vec2<Real>::T) +
-                      kBatch * static_cast<size_t>(P.w2 | 1) * sizeof(Real) + kBatch * sizeof(int);
+                      kBatch * static_cast<size_t>(P.w2 + 1) * sizeof(Real) + kBatch * sizeof(int);
   static bool configured = false;
   if (!configured) {
     NUS_CUDA(cudaFuncSetAttribute(spread_gather_kernel<Real, KG>,
@@ -190,13 +186,12 @@ template <typename Real>
 void spread_typed(const Plan& plan, const SpreadArgs& a, cudaStream_t s) {
   const PlanParams& p = plan.p;
   const SpreadTables& tb = plan.tab;
-  require(tb.tile == kThreads * kCellsPerThread || p.mr < kThreads * kCellsPerThread,
-          "spread: unexpected tile size");
+  require(tb.tile == kTile || p.mr < kTile, "spread: unexpected tile size");
   require(2 * p.w <= kMaxW2, "spread: spread width too large");
   SpreadParams<Real> P{};
   P.start = tb.start.as<int32_t>();
   P.perm = tb.perm.as<int32_t>();
-  P.frac = tb.frac.as<Real>();
+  P.gauss = tb.gauss.as<typename Vec2<Real>::T>();
   P.prephase = tb.prephase.as<Real>();
   P.ranges = tb.tile_range.as<int32_t>();
   P.wrap_lo = tb.wrap_lo.as<int32_t>();
