@@ -11,11 +11,46 @@ NVFLAGS  := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC \
             --expt-relaxed-constexpr -Iinclude -I$(SRC) -Xptxas -warn-spills
 HDRS     := include/nus_c.h $(SRC)/nus_internal.cuh $(SRC)/nus_estimator.cuh
 
-.PHONY: all lib oracle clean
+.PHONY: all lib cpp oracle reftests clean
 
-all: lib oracle
+all: lib cpp oracle
 
 lib: $(LIBDIR)/libnus_b200.so
+
+# C++ drop-in (include/nuspectral/*.hpp) over the C-ABI
+CXX        ?= g++
+HOST_SRCS  := $(wildcard $(SRC)/host/*.cpp)
+HOST_OBJS  := $(patsubst $(SRC)/host/%.cpp,build/host/%.o,$(HOST_SRCS))
+CXXFLAGS   := -std=c++20 -O2 -fPIC -Wall -Wextra -Iinclude -I$(SRC)/host
+cpp: $(LIBDIR)/libnuspectral_b200.so
+
+build/host/%.o: $(SRC)/host/%.cpp $(wildcard include/nuspectral/*.hpp) include/nus_c.h $(SRC)/host/status.hpp
+	@mkdir -p build/host
+	$(CXX) $(CXXFLAGS) -c -o $@ $<
+
+$(LIBDIR)/libnuspectral_b200.so: $(HOST_OBJS) $(LIBDIR)/libnus_b200.so
+	$(CXX) -shared -o $@ $(HOST_OBJS) -L$(LIBDIR) -lnus_b200 -Wl,-rpath,'$$ORIGIN'
+
+# The reference's own doctest files compiled UNCHANGED against the drop-in headers
+# (test infrastructure; needs /root/reference, outputs travel in oracle/_ref/dropin).
+REF       ?= /root/reference/proj
+DROPIN    := oracle/_ref/dropin
+REFTESTS  := test_nufft test_fft test_grid
+REFT_FLAGS := -std=gnu++20 -O2 -Iinclude -Itests/dropin -I$(REF)/include -I$(REF)/tests
+reftests: $(addprefix $(DROPIN)/,$(REFTESTS))
+
+$(DROPIN)/support.o: $(REF)/src/simkit.cpp $(REF)/tests/support/oracles.cpp $(REF)/src/simd_scalar.cpp $(REF)/src/simd_dispatch.cpp
+	@mkdir -p $(DROPIN)
+	$(CXX) $(REFT_FLAGS) -c -o $(DROPIN)/simkit.o $(REF)/src/simkit.cpp
+	$(CXX) $(REFT_FLAGS) -c -o $(DROPIN)/oracles.o $(REF)/tests/support/oracles.cpp
+	$(CXX) $(REFT_FLAGS) -c -o $(DROPIN)/simd_scalar.o $(REF)/src/simd_scalar.cpp
+	$(CXX) $(REFT_FLAGS) -c -o $(DROPIN)/simd_dispatch.o $(REF)/src/simd_dispatch.cpp
+	$(CXX) $(REFT_FLAGS) -c -o $(DROPIN)/test_main.o $(REF)/tests/test_main.cpp
+	ld -r -o $@ $(DROPIN)/simkit.o $(DROPIN)/oracles.o $(DROPIN)/simd_scalar.o $(DROPIN)/simd_dispatch.o $(DROPIN)/test_main.o
+
+$(DROPIN)/%: $(REF)/tests/%.cpp $(DROPIN)/support.o $(LIBDIR)/libnuspectral_b200.so tests/dropin/doctest.h
+	$(CXX) $(REFT_FLAGS) -o $@ $< $(DROPIN)/support.o -L$(LIBDIR) -lnuspectral_b200 -lnus_b200 \
+	    -Wl,-rpath,'$$ORIGIN/../../../$(LIBDIR)' -pthread
 
 build/cu/%.o: $(SRC)/%.cu $(HDRS)
 	@mkdir -p build/cu

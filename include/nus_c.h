@@ -97,6 +97,13 @@ int nus_plan_execute_device(nus_plan_t plan, const void* y_dev, int64_t batch, v
 int nus_ndft_direct(const double* times, int64_t n, const double* y_host, const double* centers,
                     int64_t n_centers, int32_t device, double* out_host);
 
+/* In-place forward (inverse != 0: unscaled inverse) complex FFT of n (power of two)
+ * interleaved fp64 values on the device (Radix2Fft, fft.hpp:12-29 / fft.cpp:39-58). */
+int nus_fft_inplace(double* data_host, int64_t n, int32_t inverse, int32_t device);
+/* Dense R(B) (n x n row-major) filled on the device (signal_band_kernel, kernels.cpp:100-115). */
+int nus_signal_band_matrix(const double* times, int64_t n, double f_max, int32_t device,
+                           double* out_host);
+
 /* ---- tapers (tapers.hpp) -------------------------------------------------- */
 /* Top-k eigenpairs of the commuting tridiagonal (tapers.cpp:40-52); vectors K x n unit norm,
  * largest-|v| entry positive (eig.cpp:281-289).  eigenvalues / concentrations may be NULL. */

@@ -93,6 +93,8 @@ _SIGS = {
     "nus_plan_execute": [_vp, _dp, _i64, _dp],
     "nus_plan_execute_device": [_vp, _vp, _i64, _vp, _vp],
     "nus_ndft_direct": [_dp, _i64, _dp, _dp, _i64, _i32, _dp],
+    "nus_fft_inplace": [_dp, _i64, _i32, _i32],
+    "nus_signal_band_matrix": [_dp, _i64, _d, _i32, _dp],
     "nus_dpss": [_i64, _d, _i64, _i32, _dp, _dp, _dp],
     "nus_tridiagonal_eigen": [_dp, _dp, _i64, _i64, _i32, _dp, _dp, _dp],
     "nus_signal_band_quadform": [_dp, _i64, _d, _dp, _i64, _i64, _i64, _i32, _dp],

@@ -213,6 +213,59 @@ int nus_ndft_direct(const double* times, int64_t n, const double* y_host, const 
   });
 }
 
+namespace {
+__global__ void signal_band_matrix_kernel(const double* __restrict__ t, int64_t n, double f,
+                                          double tol, double* __restrict__ m) {
+  const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (g >= n * n) return;
+  const int64_t r = g / n, c = g - r * n;
+  double v;
+  if (r == c) {
+    v = 2.0 * f;
+  } else {
+    const double d = t[r] - t[c];
+    v = fabs(d) < tol ? 2.0 * f : sin(2.0 * nus::kPi * f * d) / (nus::kPi * d);  // kernels.cpp:16-19
+  }
+  m[g] = v;
+}
+}  // namespace
+
+int nus_fft_inplace(double* data_host, int64_t n, int32_t inverse, int32_t device) {
+  return guarded([&] {
+    nus::require(data_host != nullptr, "Radix2Fft: null data");
+    nus::require(n > 0 && (n & (n - 1)) == 0, "Radix2Fft: size must be a power of two");
+    nus::use_device(device);
+    nus::DeviceBuffer d(n * 2 * sizeof(double));
+    NUS_CUDA(cudaMemcpy(d.ptr, data_host, d.bytes, cudaMemcpyHostToDevice));
+    if (n > 1) {
+      cufftHandle h;
+      NUS_CUFFT(cufftPlan1d(&h, static_cast<int>(n), CUFFT_Z2Z, 1));
+      const cufftResult r = cufftExecZ2Z(h, d.as<cufftDoubleComplex>(), d.as<cufftDoubleComplex>(),
+                                         inverse ? CUFFT_INVERSE : CUFFT_FORWARD);
+      cufftDestroy(h);
+      NUS_CUFFT(r);
+    }
+    NUS_CUDA(cudaMemcpy(data_host, d.ptr, d.bytes, cudaMemcpyDeviceToHost));
+  });
+}
+
+int nus_signal_band_matrix(const double* times, int64_t n, double f_max, int32_t device,
+                           double* out_host) {
+  return guarded([&] {
+    nus::require(times && out_host, "signal_band_kernel: null argument");
+    nus::require(n >= 1, "signal_band_kernel: empty grid");
+    nus::use_device(device);
+    nus::DeviceBuffer t(n * sizeof(double)), m(static_cast<size_t>(n) * n * sizeof(double));
+    NUS_CUDA(cudaMemcpy(t.ptr, times, t.bytes, cudaMemcpyHostToDevice));
+    const double mean_dt = n > 0 ? (times[n - 1] - times[0]) / static_cast<double>(n) : 0.0;
+    signal_band_matrix_kernel<<<static_cast<unsigned>((n * n + 255) / 256), 256>>>(
+        t.as<double>(), n, f_max, 1e-12 * mean_dt, m.as<double>());
+    nus::note_launch();
+    nus::check_launch("signal_band_matrix_kernel");
+    NUS_CUDA(cudaMemcpy(out_host, m.ptr, m.bytes, cudaMemcpyDeviceToHost));
+  });
+}
+
 // ---- tapers -----------------------------------------------------------------------
 
 int nus_dpss(int64_t n, double tw, int64_t k, int32_t device, double* tapers_host,
