@@ -1,0 +1,241 @@
+"""Multi-GPU partitioning of the MTNUFFT path, one process per GPU.
+
+Three shardings, all driven by ``torch.distributed`` (NCCL over NVLink/NVSwitch on
+the B200 box; ``gloo`` in the CPU tests):
+
+* :class:`ChannelShard` — independent channels (config C3): rank r owns channels
+  [r C/G, (r+1) C/G) with their own tapers, plans and grids.  No data-path
+  collective; P can optionally be all-gathered.
+* :class:`TaperShard` — independent tapers of one series: rank r spreads all N
+  samples for its taper subset and reduces sum_k |J_k|^2 (one ``reduce`` of I reals).
+* :class:`SampleSplit` — one very long series (config C4): rank r owns a
+  contiguous chunk of the time-sorted samples, spreads it into a FULL local
+  fine grid for all K tapers (K padded to a multiple of G), then one in-place
+  ``reduce_scatter`` (sum) hands rank r the complete grids of tapers
+  [r K_pad/G, (r+1) K_pad/G); it FFTs + crops those and a final ``reduce``
+  sums the partial spectra.  Taper normalisation is row-split too: each rank
+  computes its rows of w^T R(B) w and the K partial sums are all-reduced.
+
+The device work goes through an *engine* (``DeviceEngine`` = the C-ABI on this
+rank's GPU); the orchestration only moves torch tensors through collectives.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _capi as C
+
+
+def split_range(n: int, world: int, rank: int):
+    """Contiguous near-equal split of [0, n)."""
+    return n * rank // world, n * (rank + 1) // world
+
+
+def balanced_triangle_rows(n: int, world: int):
+    """Row boundaries so each rank gets ~equal work in the upper-triangle sum
+    sum_n (2F w_n^2 + 2 sum_{m>n} ...): row n costs (n_total - n) pairs."""
+    total = n * (n + 1) / 2.0
+    bounds = [0]
+    for g in range(1, world):
+        # solve sum_{i<r} (n - i) = g/world * total  ->  r n - r(r-1)/2 = target
+        target = total * g / world
+        r = (2 * n + 1 - math.sqrt((2 * n + 1) ** 2 - 8 * target)) / 2
+        bounds.append(int(min(max(round(r), bounds[-1]), n)))
+    bounds.append(n)
+    return bounds
+
+
+# --------------------------------------------------------------------------- engine
+
+class DeviceEngine:
+    """One rank's GPU work through the C-ABI (libnus_b200.so)."""
+
+    def __init__(self, device: int = 0):
+        self.device = device
+        import torch
+        self.torch = torch
+        self.dev = torch.device("cuda", device)
+
+    # taper setup -------------------------------------------------------------
+    def taper_spline(self, times, f_max, f_w, k):
+        t = C.f64(times)
+        w = np.empty((k, t.size))
+        C.check(C.lib().nus_taper_spline(C.dptr(t), t.size, f_max, f_w, k, self.device, C.dptr(w)))
+        return w
+
+    def quadform_rows(self, times, f_max, w, row0, row1):
+        t, w = C.f64(times), C.f64(w)
+        q = np.empty(w.shape[0])
+        C.check(C.lib().nus_signal_band_quadform(C.dptr(t), t.size, f_max, C.dptr(w), w.shape[0], row0,
+                                                 row1, self.device, C.dptr(q)))
+        return q
+
+    # estimator ---------------------------------------------------------------
+    def create(self, times, centers, f_max, f_w, k, eps, precision, tapers):
+        from .api import _Estimator
+        return _Estimator(times, centers, f_max, f_w, k, eps, 1, precision, self.device, tapers=tapers)
+
+    def real_dtype(self, est):
+        return self.torch.float32 if est.info.precision == C.F32 else self.torch.float64
+
+    def zeros(self, shape, dtype):
+        return self.torch.zeros(shape, dtype=dtype, device=self.dev)
+
+    def to_device(self, a, dtype):
+        return self.torch.as_tensor(np.ascontiguousarray(a), dtype=dtype, device=self.dev)
+
+    def _stream(self):
+        return self.torch.cuda.current_stream(self.dev).cuda_stream
+
+    def estimate(self, est, x, power):
+        C.check(C.lib().nus_mtnufft_estimate_device(est.h, x.data_ptr(), 1 if x.dtype == self.torch.float32 else 0,
+                                                    power.data_ptr(), None, self._stream()))
+
+    def spread(self, est, x, s0, s1, grid, kpad):
+        C.check(C.lib().nus_mtnufft_spread_device(est.h, x.data_ptr(), 1 if x.dtype == self.torch.float32 else 0,
+                                                  s0, s1, grid.data_ptr(), kpad, self._stream()))
+
+    def transform(self, est, grid_rows, k0, k1, divisor, power):
+        C.check(C.lib().nus_mtnufft_transform_device(est.h, grid_rows.data_ptr(), k0, k1, divisor, 0,
+                                                     power.data_ptr(), self._stream()))
+
+    def mr(self, est):
+        return int(est.info.mr)
+
+
+# --------------------------------------------------------------------------- shardings
+
+class ChannelShard:
+    """Config C3: channels sharded across ranks, no data-path collective."""
+
+    def __init__(self, times, centers, f_max, f_w, k, eps, precision="f32", engine=None, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.group = group
+        times = np.atleast_2d(times)
+        self.channels = times.shape[0]
+        self.c0, self.c1 = split_range(self.channels, self.world, self.rank)
+        self.engine = engine or DeviceEngine()
+        f_w = np.broadcast_to(np.asarray(f_w, dtype=np.float64), (self.channels,))
+        self.est = None
+        if self.c1 > self.c0:
+            # one batch estimator per rank: channels share n, centres, K, eps (tapers are per channel)
+            self.est = self.engine.create(times[self.c0:self.c1], centers, f_max, float(f_w[self.c0]), k, eps,
+                                          precision, None)
+        self.nc = len(centers)
+
+    def estimate_local(self, x_local, power_local):
+        """x_local: this rank's channels [c1-c0][n] on the device."""
+        if self.est is not None:
+            self.engine.estimate(self.est, x_local, power_local)
+
+    def gather(self, power_local):
+        """All-gather P of every channel (optional; the throughput path never calls it)."""
+        import torch
+        counts = [split_range(self.channels, self.world, r) for r in range(self.world)]
+        width = max(b - a for a, b in counts)  # collectives need equal shapes: pad, then trim
+        padded = torch.zeros((width, self.nc), dtype=power_local.dtype, device=power_local.device)
+        padded[: power_local.shape[0]] = power_local
+        bufs = [torch.empty_like(padded) for _ in counts]
+        self.dist.all_gather(bufs, padded, group=self.group)
+        return torch.cat([buf[: b - a] for buf, (a, b) in zip(bufs, counts)], dim=0)
+
+
+class TaperShard:
+    """One series, tapers sharded: rank r spreads all samples for its tapers, then reduce(P)."""
+
+    def __init__(self, times, centers, f_max, f_w, tapers, eps, precision="f64", engine=None, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.group = group
+        self.k = tapers.shape[0]
+        self.k0, self.k1 = split_range(self.k, self.world, self.rank)
+        self.engine = engine or DeviceEngine()
+        self.est = None
+        if self.k1 > self.k0:
+            self.est = self.engine.create(times, centers, f_max, f_w, self.k1 - self.k0, eps, precision,
+                                          tapers[self.k0:self.k1])
+        self.nc = len(centers)
+
+    def estimate(self, x, power):
+        """x: full series on the device; power: [I] buffer; rank 0 receives P (sum / K)."""
+        if self.est is not None:
+            self.engine.estimate(self.est, x, power)  # mean over local tapers
+            power.mul_(float(self.k1 - self.k0))
+        else:
+            power.zero_()
+        self.dist.reduce(power, dst=0, op=self.dist.ReduceOp.SUM, group=self.group)
+        if self.rank == 0:
+            power.div_(float(self.k))
+        return power
+
+
+class SampleSplit:
+    """Config C4: one long series, samples split across ranks, reduce-scatter of fine grids."""
+
+    def __init__(self, times, centers, f_max, f_w, k, eps, precision="f64", engine=None, group=None,
+                 tapers: Optional[np.ndarray] = None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.group = group
+        self.engine = engine or DeviceEngine()
+        times = np.asarray(times, dtype=np.float64)
+        n = times.size
+        self.n, self.k = n, k
+        self.s0, self.s1 = split_range(n, self.world, self.rank)
+        if tapers is None:
+            tapers = self._normalised_tapers(times, f_max, f_w, k)
+        self.tapers = tapers
+        self.est = self.engine.create(times[self.s0:self.s1], centers, f_max, f_w, k, eps, precision,
+                                      tapers[:, self.s0:self.s1])
+        self.kpad = int(math.ceil(k / self.world)) * self.world
+        self.per_rank = self.kpad // self.world
+        self.mr = self.engine.mr(self.est)
+        self.real = self.engine.real_dtype(self.est)
+        # full local grid [kpad][Mr] complex as interleaved reals; padding rows stay zero
+        self.grid = self.engine.zeros((self.kpad, self.mr * 2), self.real)
+        self.owned = self.engine.zeros((self.per_rank, self.mr * 2), self.real)
+        self.nc = len(centers)
+
+    def _normalised_tapers(self, times, f_max, f_w, k):
+        """Interpolated DPSS on the full grid + row-split R(B) normalisation (all_reduce of K sums)."""
+        import torch
+        w = self.engine.taper_spline(times, f_max, f_w, k)
+        rows = balanced_triangle_rows(times.size, self.world)
+        q = np.zeros(k)
+        for k0 in range(0, k, 8):
+            q[k0:k0 + 8] = self.engine.quadform_rows(times, f_max, w[k0:k0 + 8], rows[self.rank],
+                                                     rows[self.rank + 1])
+        qt = torch.tensor(q, dtype=torch.float64)
+        if self.engine.__class__.__name__ == "DeviceEngine":
+            qt = qt.to(self.engine.dev)
+        self.dist.all_reduce(qt, op=self.dist.ReduceOp.SUM, group=self.group)
+        q = qt.cpu().numpy()
+        if not np.all(q > 0):
+            raise C.NumericError("gpss_interpolated: degenerate metric norm")
+        return w * np.sqrt(2.0 * f_w / q)[:, None]
+
+    def estimate(self, x_local, power):
+        """x_local: this rank's samples [s1-s0] on the device; rank 0 receives P in ``power``."""
+        self.engine.spread(self.est, x_local, 0, self.s1 - self.s0, self.grid, self.kpad)
+        self.dist.reduce_scatter_tensor(self.owned, self.grid, op=self.dist.ReduceOp.SUM, group=self.group)
+        k0 = self.rank * self.per_rank
+        k1 = min(self.k, k0 + self.per_rank)
+        if k1 > k0:
+            self.engine.transform(self.est, self.owned, k0, k1, 1.0, power)
+        else:
+            power.zero_()
+        self.dist.reduce(power, dst=0, op=self.dist.ReduceOp.SUM, group=self.group)
+        if self.rank == 0:
+            power.div_(float(self.k))
+        return power

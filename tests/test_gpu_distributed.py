@@ -1,0 +1,63 @@
+"""GPU: the distributed shardings through the real DeviceEngine (C-ABI spread/transform
+building blocks + NCCL collectives) in a world-size-1 NCCL group (gpurun gives one GPU).
+The multi-rank partitioning itself is covered by tests/test_distributed.py (gloo, world 2)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from conftest import rel_l2
+from oracle import C
+from paper_2407_01943_b200 import distributed as D
+from paper_2407_01943_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def nccl_group():
+    import torch
+    import torch.distributed as dist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    yield dist
+    dist.destroy_process_group()
+
+
+def test_sample_split_device_engine(nccl_group):
+    import torch
+    wl = W.small(n=20000, n_centers=8192, k=5, nw=3.0, eps=1e-9, seed=3)
+    ss = D.SampleSplit(wl.times, wl.centers, wl.f_max, float(wl.f_w[0]), 5, 1e-9)
+    x = torch.as_tensor(wl.values, device="cuda")
+    p = torch.zeros(wl.centers.size, dtype=torch.float64, device="cuda")
+    ss.estimate(x, p)
+    ref = C.mtnufft_power(wl.times, ss.tapers, wl.values, wl.centers, 1e-9)
+    assert rel_l2(p.cpu().numpy(), ref) < 1e-10
+    w_ref, _ = C.gpss_interpolated(wl.times, wl.f_max, float(wl.f_w[0]), 5)
+    assert np.abs(np.abs(ss.tapers) - np.abs(w_ref)).max() < 1e-9 * np.abs(w_ref).max()
+
+
+def test_taper_and_channel_shard_device_engine(nccl_group):
+    import torch
+    wl = W.small(n=20000, n_centers=8192, k=4, nw=2.5, eps=1e-9, seed=4)
+    w, _ = C.gpss_interpolated(wl.times, wl.f_max, float(wl.f_w[0]), 4)
+    ts = D.TaperShard(wl.times, wl.centers, wl.f_max, float(wl.f_w[0]), w, 1e-9)
+    p = torch.zeros(wl.centers.size, dtype=torch.float64, device="cuda")
+    ts.estimate(torch.as_tensor(wl.values, device="cuda"), p)
+    assert rel_l2(p.cpu().numpy(), C.mtnufft_power(wl.times, w, wl.values, wl.centers, 1e-9)) < 1e-10
+    c3 = W.c3(channels=3, n=1 << 14)
+    centers = 2500.0 * np.arange(1 << 13) / ((1 << 13) - 1)
+    cs = D.ChannelShard(c3.times, centers, 2500.0, c3.f_w, 9, 1e-5, precision="f32")
+    pl = torch.zeros((3, centers.size), dtype=torch.float32, device="cuda")
+    cs.estimate_local(torch.as_tensor(c3.values, dtype=torch.float32, device="cuda"), pl)
+    allp = cs.gather(pl).cpu().numpy()
+    wc = cs.est.tapers()
+    for ch in range(3):
+        ref = C.mtnufft_power(c3.times[ch], wc[ch], c3.values[ch], centers, 1e-9)
+        assert rel_l2(allp[ch], ref) <= 1e-4
