@@ -1,0 +1,441 @@
+// Two-pass (four-step) power-of-two FFT of the K oversampled grids with the
+// deconvolve / crop / eigenspectrum reduction fused into the second pass.
+//
+// Replaces Radix2Fft::forward (src/fft.cpp:39-58) + the crop of
+// src/nufft.cpp:161-164 + the power loop of src/estimators.cpp:113-117.
+//
+//   Mr = R * C, j = j1 C + j2, k = k1 + R k2:
+//   X[k1 + R k2] = sum_j2 w_C^{j2 k2} [ w_Mr^{j2 k1} sum_j1 x[j1 C + j2] w_R^{j1 k1} ]
+//
+// Pass A (fft_cols_kernel): each CTA loads a block of columns (CW consecutive j2,
+//   all R rows: 64-256 B contiguous per row), runs the length-R FFTs in shared
+//   memory, applies the inter-pass twiddle w_Mr^{j2 k1} (two-level table) and
+//   stores the result in place (row k1).
+// Pass B (fft_rows_crop_kernel): each CTA owns RPC consecutive rows k1 and loops
+//   over the K tapers: length-C FFT in shared memory, then for every output bin
+//   k = k1 + R k2 that the crop keeps (m = (-k) mod Mr in [-I/2, I/2)) it adds
+//   |X|^2 into a per-thread register accumulator; after the last taper it writes
+//   P(i) = d_i^2 * sum_k |X_k|^2 / K.  The transformed grid is never written back.
+//
+// In-CTA FFTs are Stockham autosort stages in shared memory with radix-16/8/4/2
+// register butterflies; every thread handles 16 elements per stage (CTA = 256
+// threads, 4096 complex elements).  Twiddles come from a per-plan table of
+// e^{-2 pi i m / L} built with sincospi (exact argument).
+#include <algorithm>
+#include <cmath>
+
+#include "nus_internal.cuh"
+
+namespace nus {
+
+namespace {
+
+constexpr int kFftThreads = 256;
+constexpr int kFftElems = 4096;  // complex elements resident per CTA
+
+template <typename Real> struct C2;
+template <> struct C2<double> { using T = double2; };
+template <> struct C2<float> { using T = float2; };
+
+template <typename T2>
+__device__ inline T2 cmul(T2 a, T2 b) {
+  return T2{a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x};
+}
+template <typename T2>
+__device__ inline T2 cadd(T2 a, T2 b) { return T2{a.x + b.x, a.y + b.y}; }
+template <typename T2>
+__device__ inline T2 csub(T2 a, T2 b) { return T2{a.x - b.x, a.y - b.y}; }
+
+// e^{-2 pi i q / 16}, q = 0..7 (cos, -sin): twiddles of the in-register butterflies
+__device__ constexpr double kW16re[8] = {1.0, 0.92387953251128674, 0.70710678118654752, 0.38268343236508977,
+                                         0.0, -0.38268343236508977, -0.70710678118654752, -0.92387953251128674};
+__device__ constexpr double kW16im[8] = {-0.0, -0.38268343236508977, -0.70710678118654752, -0.92387953251128674,
+                                         -1.0, -0.92387953251128674, -0.70710678118654752, -0.38268343236508977};
+
+template <int R>
+__host__ __device__ constexpr int bitrev_c(int i) {
+  return R <= 1 ? 0 : ((i & 1) * (R >> 1)) | bitrev_c<(R > 1 ? R / 2 : 1)>(i >> 1);
+}
+
+// Radix-2 DIT butterflies of span LEN over R registers, then the next span (template
+// recursion keeps every index a compile-time constant: no local-memory arrays).
+template <int R, int LEN, typename T2>
+__device__ inline void dit_stages(T2* v) {
+  if constexpr (LEN <= R) {
+    using Real = decltype(v[0].x);
+    constexpr int half = LEN / 2;
+#pragma unroll
+    for (int s = 0; s < R; s += LEN) {
+#pragma unroll
+      for (int q = 0; q < half; ++q) {
+        const T2 u = v[s + q];
+        T2 t = v[s + q + half];
+        constexpr int kStep = 16 / LEN;
+        const int wi = q * kStep;  // e^{-2 pi i q / LEN} = W16[wi]
+        if (wi == 4) {             // -i
+          t = T2{t.y, -t.x};
+        } else if (wi == 2) {      // (1 - i) / sqrt(2)
+          const Real c = static_cast<Real>(kW16re[2]);
+          t = T2{(t.x + t.y) * c, (t.y - t.x) * c};
+        } else if (wi == 6) {      // (-1 - i) / sqrt(2)
+          const Real c = static_cast<Real>(kW16re[2]);
+          t = T2{(t.y - t.x) * c, -(t.x + t.y) * c};
+        } else if (wi != 0) {
+          t = cmul(t, T2{static_cast<Real>(kW16re[wi]), static_cast<Real>(kW16im[wi])});
+        }
+        v[s + q] = cadd(u, t);
+        v[s + q + half] = csub(u, t);
+      }
+    }
+    dit_stages<R, LEN * 2>(v);
+  }
+}
+
+// In-register forward DFT of size R (R = 2, 4, 8, 16): natural-order in and out.
+template <int R, typename T2>
+__device__ inline void dft_reg(T2* v) {
+  using Real = decltype(v[0].x);
+  // bit-reverse permutation: swap pairs (i, bitrev(i)), indices are compile-time constants
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int j = bitrev_c<R>(i);
+    if (j > i) {
+      const T2 t = v[i];
+      v[i] = v[j];
+      v[j] = t;
+    }
+  }
+  dit_stages<R, 2>(v);
+}
+
+// Shared-memory index of logical element e.  Row buffers (pass B) use the XOR swizzle
+// e ^ ((e >> 4) & 7), which makes every Stockham stage bank-conflict free for 16-byte
+// elements (the first stage stores at stride 16); column buffers (pass A) are laid out
+// column-fastest and are conflict-free as is.
+template <bool SWZ>
+__device__ inline int sidx(int e) {
+  return SWZ ? (e ^ ((e >> 4) & 7)) : e;
+}
+
+// Register-resident FFT: the thread holds 16 elements.  Stage 0 (radix R0 in {2,4,8,16},
+// Ns = 1, no twiddles) runs on values the caller loaded straight from global memory;
+// stages 1.. are radix 16 through shared memory; the last stage's outputs stay in
+// registers for the caller's epilogue.  Thread -> butterfly mapping is column-fastest
+// (u = f + nfft * j).  On entry v[bb*R0 + q] = element (f, j + q*L/R0) of butterfly
+// u = tid + bb*256; on exit v[q] = output element (f_out, out0 + q*Ns_last).
+template <int R0, bool SWZ, typename T2>
+__device__ inline void fft16_regs(T2 (&v)[16], T2* buf, int lgL, int lgNfft, int es, int fs,
+                                  const T2* __restrict__ tw, int& f_out, int& out0, int& step_out) {
+  constexpr int B0 = 16 / R0;
+  constexpr int lgR0 = R0 == 16 ? 4 : R0 == 8 ? 3 : R0 == 4 ? 2 : 1;
+  const int nfm = (1 << lgNfft) - 1;
+  // ---- stage 0 (registers -> shared)
+  {
+    const int lgNb = lgL - lgR0;
+#pragma unroll
+    for (int bb = 0; bb < B0; ++bb) {
+      T2* g = v + bb * R0;
+      dft_reg<R0>(g);
+      const int u = threadIdx.x + bb * kFftThreads;
+      const int f = u & nfm, j = (u >> lgNfft) & ((1 << lgNb) - 1);
+      const int base = f * fs + (j << lgR0) * es;  // Ns = 1: out = j*R0 + q
+#pragma unroll
+      for (int q = 0; q < R0; ++q) buf[sidx<SWZ>(base + q * es)] = g[q];
+    }
+  }
+  __syncthreads();
+  // ---- radix-16 stages; the last keeps its outputs in registers
+  const int lgNb = lgL - 4;
+  const int u = threadIdx.x;
+  const int f = u & nfm, j = (u >> lgNfft) & ((1 << lgNb) - 1);
+  const int in0 = f * fs + j * es;
+  for (int lgNs = lgR0; lgNs < lgL; lgNs += 4) {
+    const int Ns = 1 << lgNs;
+    const int jm = j & (Ns - 1);
+    const T2 w1 = tw[jm << (lgL - lgNs - 4)];
+    T2 wq = w1;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      T2 x = buf[sidx<SWZ>(in0 + (q << lgNb) * es)];
+      if (q) {
+        x = cmul(x, wq);
+        wq = cmul(wq, w1);
+      }
+      v[q] = x;
+    }
+    dft_reg<16>(v);
+    const int outb = f * fs + (((j - jm) << 4) + jm) * es;
+    if (lgNs + 4 < lgL) {
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < 16; ++q) buf[sidx<SWZ>(outb + (q << lgNs) * es)] = v[q];
+      __syncthreads();
+    } else {
+      f_out = f;
+      out0 = ((j - jm) << 4) + jm;
+      step_out = Ns;
+    }
+  }
+}
+
+// Stage-0 input index of register slot (bb, q) for this thread: element j + q*L/R0 of FFT f.
+template <int R0>
+__device__ inline void stage0_index(int slot, int lgL, int lgNfft, int& f, int& e) {
+  constexpr int lgR0 = R0 == 16 ? 4 : R0 == 8 ? 3 : R0 == 4 ? 2 : 1;
+  const int bb = slot / R0, q = slot % R0;
+  const int lgNb = lgL - lgR0;
+  const int u = threadIdx.x + bb * kFftThreads;
+  f = u & ((1 << lgNfft) - 1);
+  const int j = (u >> lgNfft) & ((1 << lgNb) - 1);
+  e = j + (q << lgNb);
+}
+
+// ---- pass A ----------------------------------------------------------------------------
+
+template <typename Real, int R0>
+__global__ void __launch_bounds__(kFftThreads, 2) fft_cols_kernel(
+    typename C2<Real>::T* __restrict__ grid, int64_t mr, int R, int C, int CW, int64_t row_stride,
+    int rows_per_ch, int kpad, const typename C2<Real>::T* __restrict__ tw_r,
+    const typename C2<Real>::T* __restrict__ tw_hi, const typename C2<Real>::T* __restrict__ tw_lo,
+    int lo_bits) {
+  using T2 = typename C2<Real>::T;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T2* const buf = reinterpret_cast<T2*>(smem_raw);  // [R][CW]
+  const int j2_0 = blockIdx.x * CW;
+  const int64_t ch = blockIdx.y;
+  const int lgR = __ffs(R) - 1, lgCW = __ffs(CW) - 1;
+  const int64_t lo_mask = (int64_t{1} << lo_bits) - 1;
+  for (int kk = 0; kk < rows_per_ch; ++kk) {
+    T2* g = grid + (ch * kpad + kk) * row_stride;
+    T2 v[16];
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {  // coalesced: consecutive threads take consecutive columns
+      int f, e;
+      stage0_index<R0>(s, lgR, lgCW, f, e);
+      v[s] = g[static_cast<int64_t>(e) * C + j2_0 + f];
+    }
+    int f, out0, step;
+    fft16_regs<R0, false>(v, buf, lgR, lgCW, CW, 1, tw_r, f, out0, step);
+    const int64_t j2 = j2_0 + f;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int k1 = out0 + q * step;
+      const int64_t a = (j2 * k1) & (mr - 1);  // inter-pass twiddle w_Mr^{j2 k1}
+      const T2 w = cmul(tw_hi[a >> lo_bits], tw_lo[a & lo_mask]);
+      g[static_cast<int64_t>(k1) * C + j2] = cmul(v[q], w);
+    }
+    __syncthreads();  // buf reused by the next taper
+  }
+}
+
+// ---- pass B + crop / power ---------------------------------------------------------------
+
+template <typename Real, typename PReal, int R0>
+__global__ void __launch_bounds__(kFftThreads, 2) fft_rows_crop_kernel(
+    const typename C2<Real>::T* __restrict__ grid, int64_t mr, int R, int C, int RPC, int64_t kpad,
+    int k_count, int64_t nc, int64_t mode_offset, const Real* __restrict__ deconv,
+    const typename C2<Real>::T* __restrict__ tw_c, typename C2<Real>::T* __restrict__ j_out,
+    PReal* __restrict__ power, double divisor, int accumulate) {
+  using T2 = typename C2<Real>::T;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T2* const buf = reinterpret_cast<T2*>(smem_raw);  // [C] (swizzled)
+  const int k1 = blockIdx.x;                        // one row per CTA
+  const int64_t ch = blockIdx.y;
+  const int lgC = __ffs(C) - 1;
+  Real acc[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) acc[q] = Real(0);
+  int f = 0, out0 = 0, step = 1;
+  for (int kk = 0; kk < k_count; ++kk) {
+    const T2* g = grid + (ch * kpad + kk) * mr + static_cast<int64_t>(k1) * C;
+    T2 v[16];
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+      int ff, e;
+      stage0_index<R0>(s, lgC, 0, ff, e);
+      v[s] = g[e];
+    }
+    fft16_regs<R0, true>(v, buf, lgC, 0, 1, C, tw_c, f, out0, step);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const T2 x = v[q];
+      acc[q] += x.x * x.x + x.y * x.y;
+      if (j_out) {
+        const int64_t k = static_cast<int64_t>(k1) + static_cast<int64_t>(R) * (out0 + q * step);
+        int64_t i = -1;
+        if (k <= mode_offset) i = mode_offset - k;
+        else if (mr - k < nc - mode_offset) i = mode_offset + (mr - k);
+        if (i >= 0 && i < nc) {
+          const Real d = deconv[i];
+          j_out[(ch * k_count + kk) * nc + i] = T2{d * x.x, d * x.y};
+        }
+      }
+    }
+    __syncthreads();  // buf reused by the next taper
+  }
+  if (!power) return;
+  // crop (nufft.cpp:131-140): bin k = k1 + R k2 keeps i = m + I/2 for m in [-I/2, I - I/2), (-m) mod Mr = k
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int64_t k = static_cast<int64_t>(k1) + static_cast<int64_t>(R) * (out0 + q * step);
+    int64_t i = -1;
+    if (k <= mode_offset) i = mode_offset - k;
+    else if (mr - k < nc - mode_offset) i = mode_offset + (mr - k);
+    if (i >= 0 && i < nc) {
+      const double d = static_cast<double>(deconv[i]);
+      const PReal val = static_cast<PReal>(d * d * static_cast<double>(acc[q]) / divisor);
+      PReal* dst = power + ch * nc + i;
+      *dst = accumulate ? *dst + val : val;
+    }
+  }
+  (void)f;
+  (void)RPC;
+}
+
+template <typename Real>
+__global__ void twiddle_table_kernel(typename C2<Real>::T* __restrict__ out, int64_t count, int64_t stride,
+                                     int64_t denom) {
+  const int64_t m = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (m >= count) return;
+  // e^{-2 pi i (m * stride) / denom}, argument reduced exactly (powers of two)
+  const int64_t a = (m * stride) & (denom - 1);
+  double sn, cs;
+  sincospi(-2.0 * static_cast<double>(a) / static_cast<double>(denom), &sn, &cs);
+  out[m] = typename C2<Real>::T{static_cast<Real>(cs), static_cast<Real>(sn)};
+}
+
+int ilog2(int64_t v) {
+  int b = 0;
+  while ((int64_t{1} << b) < v) ++b;
+  return b;
+}
+
+}  // namespace
+
+bool fused_fft_supported(const PlanParams& p) {
+  // 4096-element in-CTA FFTs need >= 2 stages per pass: C = 4096 rows, R = Mr / 4096 = 1 or >= 32
+  return p.mr == kFftElems || (p.mr >= (int64_t{1} << 17) && p.mr <= (int64_t{1} << 24));
+}
+
+void fused_fft_prepare(Plan& plan) {
+  PlanParams& p = plan.p;
+  FusedFft& f = plan.ffft;
+  if (!fused_fft_supported(p) || f.ready) return;
+  const int lg = ilog2(p.mr);
+  // 256 threads x 16 registers: every in-CTA FFT holds exactly 4096 elements.
+  // Rows: C = 4096 (pass B, one row per CTA); columns: R = Mr / 4096 with CW = 4096 / R
+  // consecutive columns per CTA (>= 128-byte row segments for R <= 512).
+  f.C = kFftElems;
+  f.R = static_cast<int>(p.mr / f.C);
+  f.RPC = 1;
+  f.CW = f.R > 1 ? kFftElems / f.R : 0;
+  f.lo_bits = lg / 2;
+  const bool f64 = p.precision == NUS_F64;
+  const size_t cb = f64 ? sizeof(double2) : sizeof(float2);
+  const int64_t hi_count = (p.mr >> f.lo_bits), lo_count = int64_t{1} << f.lo_bits;
+  f.tw_r.alloc(std::max(f.R, 2) * cb);
+  f.tw_c.alloc(f.C * cb);
+  f.tw_hi.alloc(hi_count * cb);
+  f.tw_lo.alloc(lo_count * cb);
+  auto build = [&](DeviceBuffer& b, int64_t count, int64_t stride, int64_t denom) {
+    if (f64)
+      twiddle_table_kernel<double><<<static_cast<unsigned>((count + 255) / 256), 256>>>(b.as<double2>(), count,
+                                                                                          stride, denom);
+    else
+      twiddle_table_kernel<float><<<static_cast<unsigned>((count + 255) / 256), 256>>>(b.as<float2>(), count,
+                                                                                        stride, denom);
+    note_launch();
+    check_launch("twiddle_table_kernel");
+  };
+  build(f.tw_r, std::max(f.R, 2), 1, std::max(f.R, 2));
+  build(f.tw_c, f.C, 1, f.C);
+  build(f.tw_hi, hi_count, lo_count, p.mr);
+  build(f.tw_lo, lo_count, 1, p.mr);
+  static bool configured = false;
+  if (!configured) {
+    const int smem = kFftElems * static_cast<int>(sizeof(double2));
+#define NUS_ATTR(KERN) NUS_CUDA(cudaFuncSetAttribute(KERN, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))
+    NUS_ATTR((fft_cols_kernel<double, 16>));
+    NUS_ATTR((fft_cols_kernel<double, 8>));
+    NUS_ATTR((fft_cols_kernel<double, 4>));
+    NUS_ATTR((fft_cols_kernel<double, 2>));
+    NUS_ATTR((fft_rows_crop_kernel<double, double, 16>));
+#undef NUS_ATTR
+    configured = true;
+  }
+  NUS_CUDA(cudaDeviceSynchronize());
+  f.ready = true;
+}
+
+namespace {
+
+// first-stage radix so that the remaining stages are all radix 16: L = R0 * 16^m
+int first_radix(int L) {
+  int lg = 0;
+  while ((1 << lg) < L) ++lg;
+  const int r = lg % 4;
+  return r == 0 ? 16 : (1 << r);
+}
+
+template <typename Real>
+void launch_cols(const Plan& plan, void* grid, int64_t k, int64_t kpad, cudaStream_t s) {
+  const PlanParams& p = plan.p;
+  const FusedFft& f = plan.ffft;
+  using T2 = typename C2<Real>::T;
+  const dim3 ga(static_cast<unsigned>(f.C / f.CW), static_cast<unsigned>(p.channels));
+  const size_t smem = static_cast<size_t>(f.R) * f.CW * sizeof(T2);
+  auto* g = static_cast<T2*>(grid);
+  const T2 *tr = f.tw_r.as<T2>(), *th = f.tw_hi.as<T2>(), *tl = f.tw_lo.as<T2>();
+  const int r0 = first_radix(f.R);
+#define NUS_COLS(R0)                                                                                   \
+  fft_cols_kernel<Real, R0><<<ga, kFftThreads, smem, s>>>(g, p.mr, f.R, f.C, f.CW, p.mr, static_cast<int>(k), \
+                                                          static_cast<int>(kpad), tr, th, tl, f.lo_bits)
+  if (r0 == 16) NUS_COLS(16);
+  else if (r0 == 8) NUS_COLS(8);
+  else if (r0 == 4) NUS_COLS(4);
+  else NUS_COLS(2);
+#undef NUS_COLS
+}
+
+template <typename Real, typename PReal>
+void launch_rows(const Plan& plan, void* grid, int64_t k, int64_t kpad, void* j_out, void* power, double divisor,
+                 int acc, cudaStream_t s) {
+  const PlanParams& p = plan.p;
+  const FusedFft& f = plan.ffft;
+  using T2 = typename C2<Real>::T;
+  const dim3 gb(static_cast<unsigned>(f.R), static_cast<unsigned>(p.channels));
+  const size_t smem = static_cast<size_t>(f.C) * sizeof(T2);
+  auto* g = static_cast<const T2*>(grid);
+  const int r0 = first_radix(f.C);
+#define NUS_ROWS(R0)                                                                                    \
+  fft_rows_crop_kernel<Real, PReal, R0><<<gb, kFftThreads, smem, s>>>(                                  \
+      g, p.mr, f.R, f.C, 1, kpad, static_cast<int>(k), p.nc, p.mode_offset, plan.tab.deconv.as<Real>(), \
+      f.tw_c.as<T2>(), static_cast<T2*>(j_out), static_cast<PReal*>(power), divisor, acc)
+  if (r0 == 16) NUS_ROWS(16);
+  else if (r0 == 8) NUS_ROWS(8);
+  else if (r0 == 4) NUS_ROWS(4);
+  else NUS_ROWS(2);
+#undef NUS_ROWS
+}
+
+}  // namespace
+
+void run_fused_pass_a(Plan& plan, void* grid, int64_t k, int64_t kpad, cudaStream_t s) {
+  if (plan.ffft.R <= 1) return;
+  if (plan.p.precision == NUS_F64) launch_cols<double>(plan, grid, k, kpad, s);
+  else launch_cols<float>(plan, grid, k, kpad, s);
+  note_launch();
+  check_launch("fft_cols_kernel");
+}
+
+void run_fused_pass_b(Plan& plan, void* grid, int64_t k, int64_t kpad, void* j_out, void* power, bool power_f64,
+                      double divisor, bool accumulate, cudaStream_t s) {
+  const int acc = accumulate ? 1 : 0;
+  if (plan.p.precision == NUS_F64) launch_rows<double, double>(plan, grid, k, kpad, j_out, power, divisor, acc, s);
+  else if (power_f64) launch_rows<float, double>(plan, grid, k, kpad, j_out, power, divisor, acc, s);
+  else launch_rows<float, float>(plan, grid, k, kpad, j_out, power, divisor, acc, s);
+  note_launch();
+  check_launch("fft_rows_crop_kernel");
+}
+
+}  // namespace nus

@@ -105,8 +105,16 @@ class FftCache {
   std::vector<Entry> entries_;
 };
 
+// Tables of the fused two-pass FFT (fft.cu): Mr = R * C, twiddles e^{-2 pi i m / L}.
+struct FusedFft {
+  bool ready = false;
+  int R = 1, C = 1, RPC = 1, CW = 0, lo_bits = 0;
+  DeviceBuffer tw_r, tw_c, tw_hi, tw_lo;
+};
+
 struct Plan {
   PlanParams p;
+  FusedFft ffft;
   int device = 0;
   std::vector<double> times;    // host copy, time order [C][n]
   std::vector<double> centers;
@@ -147,6 +155,13 @@ void run_transform(Plan& plan, void* grid, int64_t k, int64_t kpad, void* j_out,
 void run_fft(Plan& plan, void* grid, int64_t k, int64_t kpad, cudaStream_t s);
 void run_crop(Plan& plan, void* grid, int64_t k, int64_t kpad, void* j_out, void* power,
               bool power_f64, double divisor, bool accumulate, cudaStream_t s);
+
+// Fused two-pass FFT + crop/power (fft.cu); supported for 32 <= Mr <= 2^24.
+bool fused_fft_supported(const PlanParams& p);
+void fused_fft_prepare(Plan& plan);
+void run_fused_pass_a(Plan& plan, void* grid, int64_t k, int64_t kpad, cudaStream_t s);
+void run_fused_pass_b(Plan& plan, void* grid, int64_t k, int64_t kpad, void* j_out, void* power, bool power_f64,
+                      double divisor, bool accumulate, cudaStream_t s);
 
 void launch_ndft_direct(const double* d_t, int64_t n, const void* d_y, bool y_f32,
                         const double* d_c, int64_t nc, void* d_out, bool out_f32, int64_t batch,

@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "nus_internal.cuh"
@@ -317,6 +318,8 @@ void plan_build_tables(Plan& plan, cudaStream_t st) {
   note_launch();
   check_launch("deconv_kernel");
   NUS_CUDA(cudaStreamSynchronize(st));
+  const char* fft_env = std::getenv("NUS_FFT");
+  if (!(fft_env && std::strcmp(fft_env, "cufft") == 0)) fused_fft_prepare(plan);
 }
 
 std::unique_ptr<Plan> plan_create(const double* times, int64_t channels, int64_t n,

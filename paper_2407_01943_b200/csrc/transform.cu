@@ -1,4 +1,4 @@
-// Uniform FFT of the K oversampled grids (cuFFT, batched Z2Z / C2C forward,
+// Library path (Mr > 2^24 or NUS_FFT=cufft): uniform FFT of the K oversampled grids (cuFFT, batched Z2Z / C2C forward,
 // e^{-2 pi i jk/Mr} as Radix2Fft::forward, src/fft.cpp:39-58) followed by one
 // fused deconvolve / crop / eigenspectrum kernel:
 //     J_k(i) = deconv_i * B_k[(-m_i) mod Mr],  m_i = i - I/2   (src/nufft.cpp:131-140,161-164)
@@ -45,6 +45,10 @@ __global__ void crop_power_kernel(const typename V2<Real>::T* __restrict__ grid,
 }  // namespace
 
 void run_fft(Plan& plan, void* grid, int64_t k, int64_t kpad, cudaStream_t s) {
+  if (plan.ffft.ready) {  // custom two-pass FFT: pass A here, pass B fused with the crop
+    run_fused_pass_a(plan, grid, k, kpad, s);
+    return;
+  }
   const PlanParams& p = plan.p;
   const bool f64 = p.precision == NUS_F64;
   const size_t cbytes = f64 ? sizeof(double2) : sizeof(float2);
@@ -74,6 +78,10 @@ void run_fft(Plan& plan, void* grid, int64_t k, int64_t kpad, cudaStream_t s) {
 
 void run_crop(Plan& plan, void* grid, int64_t k, int64_t kpad, void* j_out, void* power,
               bool power_f64, double divisor, bool accumulate, cudaStream_t s) {
+  if (plan.ffft.ready) {
+    run_fused_pass_b(plan, grid, k, kpad, j_out, power, power_f64, divisor, accumulate, s);
+    return;
+  }
   const PlanParams& p = plan.p;
   const bool f64 = p.precision == NUS_F64;
   const dim3 gridd(static_cast<unsigned>((p.nc + 255) / 256), static_cast<unsigned>(p.channels));
