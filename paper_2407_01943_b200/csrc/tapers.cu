@@ -71,6 +71,10 @@ __global__ void square_kernel(const double* __restrict__ e, int64_t m, double* _
 
 // ------------------------------------------------- inverse iteration (double-double)
 
+// L1 prefetch hint: the sequential sweeps below walk arrays one element per step; pulling
+// lines into L1 a few hundred bytes ahead turns ~600-cycle DRAM round trips into L1 hits.
+__device__ inline void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+
 __device__ inline uint64_t mix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
@@ -116,6 +120,11 @@ __global__ void inverse_iteration_dd_kernel(const double* __restrict__ d, const 
     dd c2 = dd_from(0.0);
     dd xi = dd_mul(x[0], scale);
     for (int64_t i = 0; i + 1 < n; ++i) {
+      if ((i & 3) == 0 && i + 96 < n) {
+        prefetch_l1(d + i + 96);
+        prefetch_l1(e + i + 96);
+        prefetch_l1(x + i + 48);
+      }
       const double sub = e[i];
       const dd ddv = dd_sub(dd_from(d[i + 1]), sig);
       const double sup = (i + 2 < n) ? e[i + 1] : 0.0;
@@ -162,6 +171,12 @@ __global__ void inverse_iteration_dd_kernel(const double* __restrict__ d, const 
       xl1 = v;
     }
     for (int64_t i = n - 2; i-- > 0;) {
+      if ((i & 3) == 0 && i >= 48) {
+        prefetch_l1(x + i - 48);
+        prefetch_l1(u + 3 * (i - 16));
+        prefetch_l1(u + 3 * (i - 20));
+        prefetch_l1(u + 3 * (i - 24));
+      }
       const dd r = dd_sub(dd_sub(x[i], dd_mul(u[3 * i + 1], xl1)), dd_mul(u[3 * i + 2], xl2));
       const dd v = dd_mul(r, u[3 * i]);
       x[i] = v;
@@ -623,7 +638,7 @@ DpssResult tridiag_top_device(const double* d_diag, const double* d_off, int64_t
   NUS_CUDA(cudaMemcpyAsync(d_sh.ptr, sig_hi.data(), k * sizeof(double), cudaMemcpyHostToDevice, s));
   NUS_CUDA(cudaMemcpyAsync(d_sl.ptr, sig_lo.data(), k * sizeof(double), cudaMemcpyHostToDevice, s));
   inverse_iteration_dd_kernel<<<static_cast<unsigned>(k), 1, 0, s>>>(
-      d_diag, d_off, n, d_sh.as<double>(), d_sl.as<double>(), 4, pivmin, xs.as<dd>(), us.as<dd>(),
+      d_diag, d_off, n, d_sh.as<double>(), d_sl.as<double>(), 3, pivmin, xs.as<dd>(), us.as<dd>(),
       d_norm.as<double>());
   note_launch();
   check_launch("inverse_iteration_dd_kernel");
