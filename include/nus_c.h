@@ -45,7 +45,8 @@ enum nus_status {
   NUS_ERR_NUMERIC = 5,          /* nuspectral::Error (numeric failure) */
   NUS_ERR_CUDA = 6,             /* CUDA / cuFFT runtime failure */
   NUS_ERR_OUT_OF_MEMORY = 7,
-  NUS_ERR_NO_DEVICE = 8
+  NUS_ERR_NO_DEVICE = 8,
+  NUS_ERR_DEGENERATE_TAPERS = 9 /* nuspectral::DegenerateTapers */
 };
 
 enum nus_path_policy { NUS_AUTO_SELECT = 0, NUS_FORCE_FAST = 1, NUS_FORCE_DIRECT = 2 };
@@ -170,6 +171,19 @@ int nus_mtnufft_transform_device(nus_mtnufft_t est, void* grid_dev, int64_t k0, 
  * [spread, fft, crop+power] and the number of runs recorded. */
 int nus_mtnufft_timing(nus_mtnufft_t est, int64_t max_runs);
 int nus_mtnufft_timing_read(nus_mtnufft_t est, double* stage_ms3, int64_t* runs);
+/* ---- inference (inference.hpp:16-48) -------------------------------------
+ * Harmonic F-test (inference.cpp:132-186) on host eigencoefficients j [K][I] complex with
+ * zero-frequency responses w0 [K] complex; outputs F [I], amplitude [I] complex, flags [I]
+ * (1 = 2 f_c <= f_w, 2 = saturated at cap).  Computed on the device. */
+int nus_f_test(const double* j_host, int64_t k, int64_t n_bands, const double* w0_host, int64_t n_samples,
+               const double* centers, double f_w, double cap, int32_t device, double* f_out, double* amp_out,
+               uint8_t* flags_out);
+/* F-test of one estimate with J kept on the device: x [channels][n] -> [channels][I] outputs. */
+int nus_mtnufft_f_test(nus_mtnufft_t est, const double* x_host, double cap, double* f_out, double* amp_out,
+                       uint8_t* flags_out);
+/* Upper-tail F(d1, d2) critical value: x with P(F > x) = p (inference.cpp:94-130). Host scalar math. */
+int nus_f_quantile(double p, int64_t d1, int64_t d2, double* out);
+
 /* Algorithmic bytes of one estimate (SURVEY §8d model) and of its spreading kernel. */
 int nus_mtnufft_bytes_model(nus_mtnufft_t est, int32_t x_dtype, double* total, double* spread,
                             double* fft, double* crop);

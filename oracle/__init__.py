@@ -348,6 +348,26 @@ class REF:
         return p, w, flags
 
     @staticmethod
+    def f_test(t, w, x, c, eps, f_max, f_w, margin=None, cap=1e12, policy=0):
+        """Reference eigencoefficients + f_test (inference.cpp:132-186)."""
+        t, w, x, c = _arr(t), _arr(np.atleast_2d(w)), _arr(x), _arr(c)
+        f = np.empty(c.size)
+        amp = np.empty(2 * c.size)
+        flags = np.empty(c.size, np.uint8)
+        crit = np.zeros(3)
+        margin = 2.0 * f_w if margin is None else margin
+        _chk(lib_ref().ref_f_test(_p(t), _i64(t.size), _p(w), _i64(w.shape[0]), _p(x), _p(c),
+                                  _i64(c.size), _d(eps), _i(policy), _d(f_max), _d(f_w), _d(margin),
+                                  _d(cap), _p(f), _p(amp), flags.ctypes.data_as(_u8p), _p(crit)))
+        return f, amp.view(np.complex128), flags, crit
+
+    @staticmethod
+    def f_quantile(p, d1, d2):
+        out = _d(0)
+        _chk(lib_ref().ref_f_quantile(_d(p), _i64(d1), _i64(d2), ctypes.byref(out)))
+        return out.value
+
+    @staticmethod
     def default_taper_count(tw):
         return int(lib_ref().ref_default_taper_count(tw))
 

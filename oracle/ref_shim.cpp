@@ -366,6 +366,40 @@ int ref_injected_power_many(void* h, const double* x, int64_t count, int threads
   });
 }
 
+// ---- inference: harmonic F-test on eigencoefficients ------
+
+int ref_f_test(const double* t, int64_t n, const double* w, int64_t k, const double* x,
+               const double* c, int64_t nc, double eps, int policy, double f_max, double f_w,
+               double margin, double cap, double* f_out, double* amp_out, uint8_t* flags,
+               double* crit /* 3 */) {
+  return guard([&] {
+    SamplingGrid g(vec(t, n));
+    std::vector<std::vector<cplx>> ws(static_cast<size_t>(k), std::vector<cplx>(n));
+    for (int64_t j = 0; j < k; ++j)
+      for (int64_t i = 0; i < n; ++i) ws[j][i] = {w[j * n + i], 0.0};
+    const TaperSet ts(g, AnalysisBand(0.0, f_w), f_max, std::move(ws), {}, true);
+    const NufftPlan p(g, vec(c, nc), eps, policy_of(policy));
+    const EigenCoefficients j = eigencoefficients(ts, SignalSeries(g, vec(x, n)), p);
+    std::vector<AnalysisBand> bands;
+    for (int64_t i = 0; i < nc; ++i) bands.emplace_back(c[i], f_w);
+    const BandPlan plan(std::move(bands), f_max, margin);
+    FTestOptions o;
+    o.saturation_cap = cap;
+    const FTestResult r = f_test(j, ts, plan, o);
+    for (int64_t i = 0; i < nc; ++i) {
+      f_out[i] = r.f_stat[i];
+      amp_out[2 * i] = r.amplitude[i].real();
+      amp_out[2 * i + 1] = r.amplitude[i].imag();
+      flags[i] = r.flags[i];
+    }
+    for (size_t q = 0; q < r.critical_values.size() && q < 3; ++q) crit[q] = r.critical_values[q].second;
+  });
+}
+
+int ref_f_quantile(double p, int64_t d1, int64_t d2, double* out) {
+  return guard([&] { *out = f_quantile(p, static_cast<size_t>(d1), static_cast<size_t>(d2)); });
+}
+
 // ---- reference RNG / grids used by the reference's own tests ---------------
 
 int ref_rng_gauss(uint64_t seed, int64_t count, double* out) {

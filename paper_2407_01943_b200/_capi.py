@@ -44,6 +44,10 @@ class NumericError(NusError):
     """nuspectral::Error raised for numeric failure."""
 
 
+class DegenerateTapers(NusError):
+    """nuspectral::DegenerateTapers (errors.hpp:36-40)."""
+
+
 class CudaError(NusError):
     pass
 
@@ -57,7 +61,7 @@ class NoDeviceError(CudaError):
 
 
 _ERRORS = {1: InvalidArgument, 2: PlanMismatch, 3: BandRangeError, 4: ExtrapolationError,
-           5: NumericError, 6: CudaError, 7: OutOfMemory, 8: NoDeviceError}
+           5: NumericError, 6: CudaError, 7: OutOfMemory, 8: NoDeviceError, 9: DegenerateTapers}
 
 _i64 = ctypes.c_int64
 _i32 = ctypes.c_int32
@@ -111,6 +115,9 @@ _SIGS = {
     "nus_mtnufft_spread_device": [_vp, _vp, _i32, _i64, _i64, _vp, _i64, _vp],
     "nus_mtnufft_transform_device": [_vp, _vp, _i64, _i64, _d, _i32, _vp, _vp],
     "nus_mtnufft_bytes_model": [_vp, _i32, _dp, _dp, _dp, _dp],
+    "nus_f_test": [_dp, _i64, _i64, _dp, _i64, _dp, _d, _d, _i32, _dp, _dp, ctypes.POINTER(ctypes.c_uint8)],
+    "nus_mtnufft_f_test": [_vp, _dp, _d, _dp, _dp, ctypes.POINTER(ctypes.c_uint8)],
+    "nus_f_quantile": [_d, _i64, _i64, _dp],
     "nus_mtnufft_timing": [_vp, _i64],
     "nus_mtnufft_timing_read": [_vp, _dp, _i64p],
 }

@@ -18,8 +18,8 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 from . import _capi as C
-from ._capi import (BandRangeError, ExtrapolationError, InvalidArgument, NoDeviceError, NusError,
-                    NumericError, PlanMismatch)
+from ._capi import (BandRangeError, DegenerateTapers, ExtrapolationError, InvalidArgument,
+                    NoDeviceError, NusError, NumericError, PlanMismatch)
 
 __all__ = [
     "SamplingGrid", "SignalSeries", "SignalBand", "AnalysisBand", "BandPlan", "make_band_plan",
@@ -28,7 +28,8 @@ __all__ = [
     "signal_band_quadform", "EigenCoefficients", "eigencoefficients", "SpectrumEstimate",
     "MtnufftEstimator", "estimate_mtnufft", "default_taper_count", "kBandBoundary", "kBandFailed",
     "NusError", "InvalidArgument", "PlanMismatch", "BandRangeError", "ExtrapolationError",
-    "NumericError", "NoDeviceError", "Precision",
+    "NumericError", "NoDeviceError", "Precision", "DegenerateTapers", "FTestResult", "FTestOptions",
+    "f_test", "f_quantile", "kFtestConditionViolated", "kFtestSaturated",
 ]
 
 kBandBoundary = 1  # grid.hpp:10
@@ -503,6 +504,15 @@ class _Estimator:
         C.check(C.lib().nus_mtnufft_estimate(self.h, C.dptr(x), C.dptr(out)))
         return out
 
+    def f_test(self, x, cap=1e12):
+        x = C.f64(x).reshape(self.channels, self.n)
+        f = np.empty((self.channels, self.nc))
+        amp = np.empty(2 * self.channels * self.nc)
+        flags = np.empty((self.channels, self.nc), np.uint8)
+        C.check(C.lib().nus_mtnufft_f_test(self.h, C.dptr(x), cap, C.dptr(f), C.dptr(amp),
+                                           flags.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))))
+        return f, amp.view(np.complex128).reshape(self.channels, self.nc), flags
+
     def eigencoefficients(self, x):
         x = C.f64(x).reshape(self.channels, self.n)
         out = np.empty(2 * self.channels * self.k * self.nc)
@@ -569,6 +579,18 @@ class MtnufftEstimator:
         j = self._est.eigencoefficients(values)[0]
         return EigenCoefficients(self._opts.k_tapers, self._plan.size(), j)
 
+    def f_test(self, values, opts: Optional["FTestOptions"] = None) -> "FTestResult":
+        """Harmonic F-test with the eigencoefficients kept on the device (inference.cpp:132-186)."""
+        opts = opts or FTestOptions()
+        v = np.asarray(values, dtype=np.float64).reshape(-1)
+        if v.size != self._grid.n_samples():
+            raise InvalidArgument("estimate: series length does not match grid")
+        if self._opts.k_tapers < 2:
+            raise InvalidArgument("f_test: need at least 2 tapers")
+        f, amp, flags = self._est.f_test(v, opts.saturation_cap)
+        return _ftest_result(self._plan, f[0], amp[0], flags[0], self._opts.k_tapers,
+                             self._grid.n_samples(), opts)
+
     def tapers(self) -> TaperSet:
         w = self._est.tapers()[0]
         return TaperSet(self._grid, AnalysisBand(0.0, self._plan.half_width()), self._plan.f_max, w)
@@ -588,3 +610,61 @@ def estimate_mtnufft(series: SignalSeries, signal_band: SignalBand, plan: BandPl
     """Cold one-shot (estimators.cpp:261-270)."""
     opts = MtnufftEstimator.Options(k_tapers=k_tapers, epsilon=epsilon, precision=precision)
     return MtnufftEstimator(series.grid, signal_band, plan, opts).estimate(series.values)
+
+
+# ---------------------------------------------------------------- inference.hpp
+
+kFtestConditionViolated = 1  # inference.hpp:16
+kFtestSaturated = 2          # inference.hpp:17
+
+
+@dataclass
+class FTestOptions:
+    p_levels: Sequence[float] = ()
+    saturation_cap: float = 1e12
+
+
+@dataclass
+class FTestResult:
+    plan: BandPlan
+    f_stat: np.ndarray
+    amplitude: np.ndarray
+    dof: tuple
+    critical_values: List[tuple]
+    flags: np.ndarray
+    saturation_cap: float
+
+
+def f_quantile(p: float, d1: int, d2: int) -> float:
+    """Upper-tail F(d1, d2) critical value (inference.cpp:94-130); host scalar math in the library."""
+    out = ctypes.c_double()
+    C.check(C.lib().nus_f_quantile(float(p), int(d1), int(d2), ctypes.byref(out)))
+    return out.value
+
+
+def _ftest_result(plan, f, amp, flags, k, n, opts):
+    levels = list(opts.p_levels) or [0.05, 0.01, 1.0 / n]
+    crit = [(p, f_quantile(p, 2, 2 * k - 2)) for p in levels]
+    return FTestResult(plan, f, amp, (2, 2 * k - 2), crit, flags, opts.saturation_cap)
+
+
+def f_test(eigencoeffs: EigenCoefficients, tapers: TaperSet, plan: BandPlan,
+           opts: Optional[FTestOptions] = None, device: int = 0) -> FTestResult:
+    """inference.cpp:132-186 on the device (host eigencoefficients in, as the reference API)."""
+    opts = opts or FTestOptions()
+    k = tapers.k_tapers()
+    if k < 2:
+        raise InvalidArgument("f_test: need at least 2 tapers")
+    if eigencoeffs.n_tapers != k or eigencoeffs.n_bands != plan.size():
+        raise InvalidArgument("f_test: eigencoefficient shape mismatch")
+    j = C.c128_as_f64(np.asarray(eigencoeffs.data, np.complex128).reshape(k, plan.size()))
+    w0 = C.c128_as_f64(tapers.zero_frequency_responses())
+    c = C.f64(plan.centers())
+    nb = plan.size()
+    f = np.empty(nb)
+    amp = np.empty(2 * nb)
+    flags = np.empty(nb, np.uint8)
+    C.check(C.lib().nus_f_test(C.dptr(j), k, nb, C.dptr(w0), tapers.n_samples(), C.dptr(c), plan.half_width(),
+                               opts.saturation_cap, device, C.dptr(f), C.dptr(amp),
+                               flags.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))))
+    return _ftest_result(plan, f, amp.view(np.complex128), flags, k, tapers.n_samples(), opts)

@@ -501,6 +501,60 @@ int nus_mtnufft_timing_read(nus_mtnufft_t est, double* stage_ms3, int64_t* runs)
   });
 }
 
+int nus_f_test(const double* j_host, int64_t k, int64_t n_bands, const double* w0_host, int64_t n_samples,
+               const double* centers, double f_w, double cap, int32_t device, double* f_out, double* amp_out,
+               uint8_t* flags_out) {
+  return guarded([&] {
+    nus::require(j_host && w0_host && centers && f_out && amp_out && flags_out, "f_test: null argument");
+    nus::require(k >= 2, "f_test: need at least 2 tapers");
+    nus::require(n_bands >= 1, "f_test: eigencoefficient shape mismatch");
+    nus::use_device(device);
+    nus::DeviceBuffer j(static_cast<size_t>(k) * n_bands * 2 * sizeof(double)), c(n_bands * sizeof(double)),
+        f(n_bands * sizeof(double)), a(n_bands * 2 * sizeof(double)), fl(n_bands);
+    NUS_CUDA(cudaMemcpy(j.ptr, j_host, j.bytes, cudaMemcpyHostToDevice));
+    NUS_CUDA(cudaMemcpy(c.ptr, centers, c.bytes, cudaMemcpyHostToDevice));
+    nus::ftest_device(j.ptr, false, k, n_bands, 1, w0_host, n_samples, c.as<double>(), f_w, cap, f.as<double>(),
+                      a.as<double>(), fl.as<uint8_t>(), 0);
+    NUS_CUDA(cudaMemcpy(f_out, f.ptr, f.bytes, cudaMemcpyDeviceToHost));
+    NUS_CUDA(cudaMemcpy(amp_out, a.ptr, a.bytes, cudaMemcpyDeviceToHost));
+    NUS_CUDA(cudaMemcpy(flags_out, fl.ptr, fl.bytes, cudaMemcpyDeviceToHost));
+  });
+}
+
+int nus_mtnufft_f_test(nus_mtnufft_t est, const double* x_host, double cap, double* f_out, double* amp_out,
+                       uint8_t* flags_out) {
+  return guarded([&] {
+    nus::require(est && x_host && f_out && amp_out && flags_out, "f_test: null argument");
+    auto& e = *est->est;
+    std::lock_guard<std::mutex> lock(e.mu);
+    nus::use_device(e.cfg.device);
+    const auto& p = e.plan->p;
+    const int64_t C = e.cfg.channels, K = e.cfg.k_tapers, nb = p.nc;
+    nus::require(K >= 2, "f_test: need at least 2 tapers");
+    const bool f32 = p.precision == NUS_F32 && p.path == NUS_PATH_FAST;
+    cudaStream_t s = e.stream();
+    nus::DeviceBuffer x(static_cast<size_t>(C) * e.cfg.n * sizeof(double));
+    nus::DeviceBuffer j(static_cast<size_t>(C) * K * nb * 2 * (f32 ? sizeof(float) : sizeof(double)));
+    NUS_CUDA(cudaMemcpyAsync(x.ptr, x_host, x.bytes, cudaMemcpyHostToDevice, s));
+    nus::estimator_run(e, x.ptr, 0, nullptr, false, j.ptr, s);  // J stays on the device
+    std::vector<double> w0(C * K * 2);
+    nus::taper_zero_frequency(e, w0.data());
+    nus::DeviceBuffer f(C * nb * sizeof(double)), a(C * nb * 2 * sizeof(double)), fl(C * nb);
+    nus::ftest_device(j.ptr, f32, K, nb, C, w0.data(), e.cfg.n, e.plan->d_centers.as<double>(), e.cfg.f_w, cap,
+                      f.as<double>(), a.as<double>(), fl.as<uint8_t>(), s);
+    NUS_CUDA(cudaMemcpy(f_out, f.ptr, f.bytes, cudaMemcpyDeviceToHost));
+    NUS_CUDA(cudaMemcpy(amp_out, a.ptr, a.bytes, cudaMemcpyDeviceToHost));
+    NUS_CUDA(cudaMemcpy(flags_out, fl.ptr, fl.bytes, cudaMemcpyDeviceToHost));
+  });
+}
+
+int nus_f_quantile(double p, int64_t d1, int64_t d2, double* out) {
+  return guarded([&] {
+    nus::require(out != nullptr, "f_quantile: null output");
+    *out = nus::f_quantile_host(p, d1, d2);
+  });
+}
+
 int nus_mtnufft_bytes_model(nus_mtnufft_t est, int32_t x_dtype, double* total, double* spread,
                             double* fft, double* crop) {
   return guarded([&] {

@@ -19,6 +19,7 @@ inline void check(int rc) {
     case NUS_ERR_BAND_RANGE: throw BandRangeError(msg);
     case NUS_ERR_EXTRAPOLATION: throw ExtrapolationError(msg);
     case NUS_ERR_NUMERIC: throw Error(msg);
+    case NUS_ERR_DEGENERATE_TAPERS: throw DegenerateTapers(msg);
     case NUS_ERR_OUT_OF_MEMORY: throw DeviceError("out of device memory: " + msg);
     default: throw DeviceError(msg);
   }

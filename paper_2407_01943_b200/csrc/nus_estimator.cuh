@@ -34,4 +34,10 @@ void estimator_timing_read(Estimator& est, double* ms3, int64_t* runs);
 void estimator_bytes(const Estimator& est, int x_dtype, double* total, double* spread, double* fft,
                      double* crop);
 
+double f_quantile_host(double p, int64_t d1, int64_t d2);
+void ftest_device(const void* j_dev, bool j_f32, int64_t k, int64_t nb, int64_t channels, const double* w0_host,
+                  int64_t n_samples, const double* d_centers, double f_w, double cap, double* f_dev,
+                  double* amp_dev, uint8_t* flags_dev, cudaStream_t s);
+void taper_zero_frequency(const Estimator& est, double* w0_host);
+
 }  // namespace nus

@@ -13,6 +13,7 @@ Every case mirrors a reference test or a BASELINE config:
   spline.npz         test_eig.cpp:252-270 sin case (max error 3.855517e-3)
   gpss.npz           gpss_interpolated on jitter / arithmetic / uniform grids (N=50)
   c1.npz             BASELINE config C1 through the full reference MtnufftEstimator (Oracle-A)
+  ftest_c1.npz       the reference f_test on C1's eigencoefficients
   bins_many_wrap.npz first_cell_ on a clustered, many-wrap grid (C4-like, 2^15 samples)
 """
 import os
@@ -103,6 +104,9 @@ def main():
     np.savez_compressed(os.path.join(HERE, "c1.npz"), t=wl.times, x=wl.values, centers=wl.centers,
                         f_max=wl.f_max, f_w=wl.f_w[0], k=wl.k, eps=wl.eps, power=p, tapers=w,
                         flags=flags, first_cells=j0)
+    # harmonic F-test on the C1 eigencoefficients (inference.cpp:132-186), reference tapers
+    f, amp, fflags, crit = REF.f_test(wl.times, w, wl.values, wl.centers, wl.eps, wl.f_max, float(wl.f_w[0]))
+    np.savez_compressed(os.path.join(HERE, "ftest_c1.npz"), f=f, amp=amp, flags=fflags, crit=crit)
 
     # many-wrap clustered grid (C4-like at 2^15 samples, 2^13 dyadic centres)
     c4 = W.c4(n=1 << 15, n_centers=1 << 13, windows=50)

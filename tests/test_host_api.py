@@ -115,3 +115,15 @@ def test_workloads_are_valid_grids(gen):
 def test_workloads_are_seeded():
     a, b = W.c2(n=4096), W.c2(n=4096)
     assert np.array_equal(a.times, b.times) and np.array_equal(a.values, b.values)
+
+
+def test_f_quantile_matches_reference_and_scipy():
+    from scipy.stats import f as fdist
+    from oracle import REF, ref_available
+    for p, d1, d2 in ((0.05, 2, 12), (0.01, 2, 12), (1 / 4096, 2, 12), (0.05, 2, 60), (0.3, 3, 7)):
+        v = nus.f_quantile(p, d1, d2)
+        assert v == pytest.approx(fdist.isf(p, d1, d2), rel=1e-9)
+        if ref_available():
+            assert v == pytest.approx(REF.f_quantile(p, d1, d2), rel=1e-10)
+    with pytest.raises(nus.InvalidArgument):
+        nus.f_quantile(1.5, 2, 3)
