@@ -90,6 +90,8 @@ struct SpreadTables {
   DeviceBuffer perm;            // int32 [C][n] original sample index of sorted point
   DeviceBuffer gauss;           // real2 [C][n] (A, g): W_p = A g^p C_p for the point's 2w cells
   DeviceBuffer prephase;        // real2 [C][n] e^{-i 2pi fshift t}
+  int64_t nseg = 0;             // 32-cell segments (tensor-core spread)
+  DeviceBuffer seg_range;       // int32 [C][nseg][4]: own lo, own hi, wrap lo, 0
   DeviceBuffer tile_range;      // int32 [C][ntiles+1][2]: point range of tile (lo, hi)
   DeviceBuffer wrap_lo;         // int32 [C]: first sorted point whose support wraps into tile 0
   DeviceBuffer deconv;          // real  [I]

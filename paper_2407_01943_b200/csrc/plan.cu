@@ -223,6 +223,23 @@ __global__ void tile_ranges_kernel(const int32_t* __restrict__ start, int64_t n,
   ranges[2 * g + 1] = lower_bound_i32(s, static_cast<int32_t>(n), c0 + tile);
 }
 
+// Point ranges of the 32-cell segments of the tensor-core spread: int32 [C][nseg][4] =
+// (own lo, own hi, wrap lo, 0): own points start in [s0-(w2-1), s0+32), wrapping points
+// (segments with s0 < w2-1 only) start in [Mr+s0-(w2-1), Mr) and run to the channel's end.
+__global__ void seg_ranges_kernel(const int32_t* __restrict__ start, int64_t n, int64_t channels, int64_t nseg,
+                                  int w2, int64_t mr, int32_t* __restrict__ ranges) {
+  const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (g >= channels * nseg) return;
+  const int64_t c = g / nseg, sg = g - c * nseg;
+  const int32_t* s = start + c * n;
+  const int64_t s0 = sg * 32;
+  ranges[4 * g] = lower_bound_i32(s, static_cast<int32_t>(n), s0 - (w2 - 1));
+  ranges[4 * g + 1] = lower_bound_i32(s, static_cast<int32_t>(n), s0 + 32);
+  ranges[4 * g + 2] = s0 < w2 - 1 ? lower_bound_i32(s, static_cast<int32_t>(n), mr + s0 - (w2 - 1))
+                                  : static_cast<int32_t>(n);
+  ranges[4 * g + 3] = 0;
+}
+
 template <typename Real>
 __global__ void deconv_kernel(int64_t nc, int64_t mode_offset, double tau, double norm,
                               Real* __restrict__ out) {
@@ -307,6 +324,15 @@ void plan_build_tables(Plan& plan, cudaStream_t st) {
         tb.tile_range.as<int32_t>(), tb.wrap_lo.as<int32_t>());
     note_launch();
     check_launch("tile_ranges_kernel");
+  }
+  tb.nseg = p.mr / 32;
+  tb.seg_range.alloc(p.channels * tb.nseg * 4 * sizeof(int32_t));
+  {
+    const int64_t cnt = p.channels * tb.nseg;
+    seg_ranges_kernel<<<static_cast<unsigned>((cnt + 255) / 256), 256, 0, st>>>(
+        tb.start.as<int32_t>(), p.n, p.channels, tb.nseg, 2 * p.w, p.mr, tb.seg_range.as<int32_t>());
+    note_launch();
+    check_launch("seg_ranges_kernel");
   }
   tb.deconv.alloc(p.nc * rs);
   if (p.precision == NUS_F64)

@@ -22,6 +22,8 @@
 // accumulators per cell live in registers.  Every cell of the grid is written
 // exactly once (zeros included), so no memset.
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 #include "nus_internal.cuh"
 
@@ -51,6 +53,8 @@ struct SpreadParams {
   typename Vec2<Real>::T* grid;  // [C][kpad][mr]
   int64_t n, mr, ntiles, kpad, k_total;
   int64_t s0, s1;
+  int64_t channels, nseg;
+  const int32_t* seg_ranges;
   int tile, w, w2, k0, kg, x_dtype, x_complex;
   Real beta, cq[kMaxW2];
 };
@@ -166,6 +170,289 @@ __global__ void __launch_bounds__(kThreads, 5) spread_gather_kernel(const Spread
   (void)lane;
 }
 
+// ---- persistent, warp-independent FP64 tensor-core spread (default) ---------------------
+// The banded product of spread_gather_kernel on mma.sync m8n8k4 f64 (DMMA): per 8-cell
+// block, G(8 cells x 8 tapers) += W(8 cells x 4 points) Z(4 points x 8 tapers); lane
+// (g, t) holds a = W(cell g, point t), b = z(point t, taper g) and accumulates G(cell g,
+// tapers 2t, 2t+1) (layout checked by tests/micro/dmma_layout.cu); one MMA for Re z, one
+// for Im z.  That is 256 complex MACs per ~11 instructions against the gather's 224 per 31,
+// so what remains is staging latency, which is hidden by making every WARP an independent,
+// persistent worker: it owns 32-cell segments (4 blocks), stages up to 32 points per round
+// (one per lane) into its private shared rows, and finds each block's point range with two
+// ballots; no CTA barrier anywhere.  The global loads of round n+1 (and the perm index of
+// round n+2, so the x gather never waits on a dependent load) are in flight while round n
+// runs on the tensor cores.
+//
+// Private tables, both [row][point] with row stride kTcRows = 36 (= 4 mod 16, so the reads
+// of lane (g, t) -- row g or 8b+g, point p0+t -- and the one-lane-per-point writes are
+// bank-conflict free): WT[cell][point] = W(cell - rel_point), zero off the support and for
+// absent points, so a block needs no masking; Z[taper][point] = (re, im).  Points 32..35
+// are the zero overrun of the last 4-point step.
+constexpr int kTcWarps = 4;       // warps per CTA (each an independent worker)
+constexpr int kTcRows = 36;       // point columns per warp: 32 + overrun
+constexpr int kTcCtasPerSm = 4;
+
+__device__ inline void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// A warp's walk over its rounds: item = channel * nseg + segment; each segment visits its
+// wrapping points (part 0, segments with s0 < w2-1) then its own (part 1), 32 at a time; a
+// segment without points still yields one empty round so that its cells are written.
+struct TcCursor {
+  int64_t item, c, seg;
+  int part, b0, hi, nb;
+  int64_t shift;
+  bool valid, last;
+};
+
+template <typename Real>
+__device__ inline void tc_settle(TcCursor& u, const SpreadParams<Real>& P, int64_t total) {
+  if (u.item >= total) {
+    u.valid = false;
+    u.nb = 0;
+    u.last = false;
+    return;
+  }
+  u.valid = true;
+  u.c = u.item / P.nseg;
+  u.seg = u.item - u.c * P.nseg;
+  const int4 r = reinterpret_cast<const int4*>(P.seg_ranges)[u.item];
+  const int64_t s0 = u.seg * 32;
+  if (r.z < static_cast<int>(P.n)) {
+    u.part = 0;
+    u.b0 = r.z;
+    u.hi = static_cast<int>(P.n);
+    u.shift = s0 + P.mr;
+  } else {
+    u.part = 1;
+    u.b0 = r.x;
+    u.hi = r.y;
+    u.shift = s0;
+  }
+  u.nb = max(0, min(32, u.hi - u.b0));
+  u.last = u.b0 + 32 >= u.hi && (u.part == 1 || r.y <= r.x);
+}
+
+template <typename Real>
+__device__ inline void tc_advance(TcCursor& u, const SpreadParams<Real>& P, int64_t total, int64_t stride) {
+  if (!u.valid) return;
+  if (u.b0 + 32 < u.hi) {
+    u.b0 += 32;
+  } else {
+    const int4 r = reinterpret_cast<const int4*>(P.seg_ranges)[u.item];
+    if (u.part == 0 && r.y > r.x) {
+      u.part = 1;
+      u.b0 = r.x;
+      u.hi = r.y;
+      u.shift = u.seg * 32;
+    } else {
+      u.item += stride;
+      tc_settle(u, P, total);
+      return;
+    }
+  }
+  u.nb = min(32, u.hi - u.b0);
+  u.last = u.b0 + 32 >= u.hi && u.part == 1;
+}
+
+template <typename Real>
+struct TcPoint {  // this lane's prefetched point of the next round: raw loads only, so the
+                  // loads stay in flight until the round is staged
+  int start, ti;
+  unsigned long long xa, xb;  // x bits (f64 re/im, or f32 pair / scalar in xa)
+  typename Vec2<Real>::T ph, ag;
+  Real w[8];
+};
+
+template <typename Real>
+__device__ inline void tc_load(TcPoint<Real>& q, int ti, const TcCursor& u, int lane, const SpreadParams<Real>& P) {
+  using R2 = typename Vec2<Real>::T;
+  q.ti = -1;
+  if (!(u.valid && lane < u.nb)) return;
+  const int64_t base = u.c * P.n;
+  const int64_t gi = base + u.b0 + lane;
+  q.ti = ti;
+  q.start = P.start[gi];
+  if (P.x_complex && P.x_dtype == 0) {
+    const ulonglong2 xv = reinterpret_cast<const ulonglong2*>(P.x)[base + ti];
+    q.xa = xv.x;
+    q.xb = xv.y;
+  } else if (P.x_complex || P.x_dtype == 0) {  // f32 pair or f64 scalar: 8 bytes
+    q.xa = reinterpret_cast<const unsigned long long*>(P.x)[base + ti];
+  } else {
+    q.xa = reinterpret_cast<const unsigned int*>(P.x)[base + ti];
+  }
+  q.ph = reinterpret_cast<const R2*>(P.prephase)[gi];
+  q.ag = P.gauss[gi];
+  if (P.tapers) {
+    const Real* tp = P.tapers + (u.c * P.k_total + P.k0) * P.n + u.b0 + lane;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (k < P.kg) q.w[k] = tp[k * P.n];
+  }
+}
+
+template <typename Real>
+__device__ inline int tc_perm(const TcCursor& u, int lane, const SpreadParams<Real>& P) {
+  return (u.valid && lane < u.nb) ? P.perm[u.c * P.n + u.b0 + lane] : 0;
+}
+
+template <typename Real>
+__global__ void __launch_bounds__(kTcWarps * 32, kTcCtasPerSm) spread_tc_kernel(const SpreadParams<Real> P) {
+  using R2 = typename Vec2<Real>::T;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int RS = kTcRows;
+  constexpr size_t kWarpBytes = (8 * RS) * sizeof(double2) + (32 * RS) * sizeof(double);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  double* scq = reinterpret_cast<double*>(smem_raw);     // C_p
+  unsigned char* mine = smem_raw + kMaxW2 * sizeof(double) + warp * kWarpBytes;
+  double2* sz = reinterpret_cast<double2*>(mine);        // [8][RS]
+  double* sw = reinterpret_cast<double*>(sz + 8 * RS);   // [32][RS]
+
+  for (int i = threadIdx.x; i < P.w2; i += blockDim.x) scq[i] = static_cast<double>(P.cq[i]);
+  for (int i = lane; i < static_cast<int>(kWarpBytes / 16); i += 32)
+    reinterpret_cast<double2*>(mine)[i] = double2{0.0, 0.0};
+  __syncthreads();
+
+  const int64_t total = P.nseg * P.channels;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * kTcWarps;
+  TcCursor cur, n1, n2;
+  cur.item = static_cast<int64_t>(blockIdx.x) * kTcWarps + warp;
+  tc_settle(cur, P, total);
+  n1 = cur;
+  tc_advance(n1, P, total, stride);
+  n2 = n1;
+  tc_advance(n2, P, total, stride);
+  TcPoint<Real> pt;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) pt.w[k] = Real(0);
+  tc_load(pt, tc_perm(cur, lane, P), cur, lane, P);
+  int perm_next = tc_perm(n1, lane, P);
+
+  double cr[4][2], ci[4][2];
+#pragma unroll
+  for (int b = 0; b < 4; ++b) cr[b][0] = cr[b][1] = ci[b][0] = ci[b][1] = 0.0;
+
+  while (cur.valid) {
+    // ---- stage round `cur`: every lane writes its point's z column and full WT column
+    const bool has = lane < cur.nb;
+    const int rel = has ? static_cast<int>(static_cast<int64_t>(pt.start) - cur.shift) : INT32_MAX;
+#pragma unroll
+    for (int i = 0; i < 32 * RS / 64; ++i) reinterpret_cast<double2*>(sw)[lane + 32 * i] = double2{0.0, 0.0};
+    __syncwarp();
+    {
+      double xr = 0.0, xi = 0.0;
+      if (P.x_complex && P.x_dtype == 0) {
+        xr = __longlong_as_double(static_cast<long long>(pt.xa));
+        xi = __longlong_as_double(static_cast<long long>(pt.xb));
+      } else if (P.x_complex) {
+        xr = __uint_as_float(static_cast<unsigned>(pt.xa));
+        xi = __uint_as_float(static_cast<unsigned>(pt.xa >> 32));
+      } else if (P.x_dtype == 0) {
+        xr = __longlong_as_double(static_cast<long long>(pt.xa));
+      } else {
+        xr = __uint_as_float(static_cast<unsigned>(pt.xa));
+      }
+      if (!has || pt.ti < P.s0 || pt.ti >= P.s1) { xr = 0.0; xi = 0.0; }
+      const double pr = static_cast<double>(pt.ph.x), pi = static_cast<double>(pt.ph.y);
+      // select, not multiply: registers of lanes without a point may hold anything (NaN)
+      const double yr = has ? xr * pr - xi * pi : 0.0, yi = has ? xr * pi + xi * pr : 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const double wk = (k < P.kg && has) ? (P.tapers ? static_cast<double>(pt.w[k]) : 1.0) : 0.0;
+        sz[k * RS + lane] = double2{wk * yr, wk * yi};
+      }
+      // WT column: W_p = A g^p C_p at cell rel + p (two interleaved recurrences)
+      if (has) {
+        const double gg = static_cast<double>(pt.ag.y), g2 = gg * gg;
+        double ae = static_cast<double>(pt.ag.x), ao = ae * gg;
+        for (int p = 0; p < P.w2; p += 2) {
+          const int c = rel + p;
+          if (static_cast<unsigned>(c) < 32u) sw[c * RS + lane] = ae * scq[p];
+          if (static_cast<unsigned>(c + 1) < 32u) sw[(c + 1) * RS + lane] = ao * scq[p + 1];
+          ae *= g2;
+          ao *= g2;
+        }
+      }
+    }
+    __syncwarp();
+    // ---- prefetch round n1 (its perm is in hand) and the perm of round n2
+    tc_load(pt, perm_next, n1, lane, P);
+    perm_next = tc_perm(n2, lane, P);
+    // ---- block ranges by ballot (rel ascends over the lanes), as 4-point slots
+    int slo[4], shi[4], smin = 8, smax = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int lo = __popc(__ballot_sync(0xffffffffu, rel < 8 * b - (P.w2 - 1)));
+      const int hi = __popc(__ballot_sync(0xffffffffu, rel < 8 * b + 8));
+      slo[b] = lo >> 2;
+      shi[b] = hi > lo ? (hi + 3) >> 2 : slo[b];
+      if (shi[b] > slo[b]) {
+        smin = min(smin, slo[b]);
+        smax = max(smax, shi[b]);
+      }
+    }
+    // ---- tensor-core product: one z fragment per slot, shared by the blocks it meets
+    const double* wg = sw + g * RS + t;
+    const double2* zg = sz + g * RS + t;
+    for (int sl = smin; sl < smax; ++sl) {
+      const double2 zb = zg[4 * sl];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        if (sl >= slo[b] && sl < shi[b]) {
+          const double a = wg[8 * b * RS + 4 * sl];
+          dmma_8x8x4(cr[b][0], cr[b][1], a, zb.x);
+          dmma_8x8x4(ci[b][0], ci[b][1], a, zb.y);
+        }
+      }
+    }
+    if (cur.last) {
+      R2* out = P.grid + (cur.c * P.kpad + P.k0) * P.mr + cur.seg * 32;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int k = 2 * t + h;
+          if (k < P.kg) out[k * P.mr + 8 * b + g] = R2{static_cast<Real>(cr[b][h]), static_cast<Real>(ci[b][h])};
+          cr[b][h] = 0.0;
+          ci[b][h] = 0.0;
+        }
+      }
+    }
+    __syncwarp();  // private tables are restaged next
+    cur = n1;
+    n1 = n2;
+    tc_advance(n2, P, total, stride);
+  }
+}
+
+template <typename Real>
+void launch_tc(const SpreadParams<Real>& P, cudaStream_t s) {
+  const size_t warp_bytes = (8 * kTcRows) * sizeof(double2) + (32 * kTcRows) * sizeof(double);
+  const size_t smem = kMaxW2 * sizeof(double) + kTcWarps * warp_bytes;
+  static int blocks_per_sm = 0, sms = 0;
+  static size_t smem_cfg = 0;
+  if (smem_cfg != smem) {
+    NUS_CUDA(cudaFuncSetAttribute(spread_tc_kernel<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    int dev = 0;
+    NUS_CUDA(cudaGetDevice(&dev));
+    NUS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    NUS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, spread_tc_kernel<Real>, kTcWarps * 32,
+                                                           smem));
+    smem_cfg = smem;
+  }
+  require(blocks_per_sm > 0, "spread: tensor-core kernel does not fit on an SM");
+  const int64_t warps = P.nseg * P.channels;
+  const int64_t grid = std::min<int64_t>((warps + kTcWarps - 1) / kTcWarps, static_cast<int64_t>(blocks_per_sm) * sms);
+  spread_tc_kernel<Real><<<static_cast<unsigned>(grid), kTcWarps * 32, smem, s>>>(P);
+  note_launch();
+  check_launch("spread_tc_kernel");
+}
+
 template <typename Real, int KG>
 void launch_group(const SpreadParams<Real>& P, int64_t channels, cudaStream_t s) {
   const size_t smem = kBatch * KG * sizeof(typename Vec2<Real>::T) +
@@ -194,6 +481,9 @@ void spread_typed(const Plan& plan, const SpreadArgs& a, cudaStream_t s) {
   P.gauss = tb.gauss.as<typename Vec2<Real>::T>();
   P.prephase = tb.prephase.as<Real>();
   P.ranges = tb.tile_range.as<int32_t>();
+  P.seg_ranges = tb.seg_range.as<int32_t>();
+  P.nseg = tb.nseg;
+  P.channels = p.channels;
   P.wrap_lo = tb.wrap_lo.as<int32_t>();
   P.tapers = static_cast<const Real*>(a.tapers);
   P.x = a.x;
@@ -215,6 +505,11 @@ void spread_typed(const Plan& plan, const SpreadArgs& a, cudaStream_t s) {
     const double qc = static_cast<double>(q) - (static_cast<double>(p.w) - 0.5);
     P.cq[q] = static_cast<Real>(std::exp(-p.beta * qc * qc));
   }
+  // NUS_SPREAD=gather selects the CUDA-core broadcast gather (kept for comparison)
+  static const bool use_tc = [] {
+    const char* e = std::getenv("NUS_SPREAD");
+    return !(e && std::strcmp(e, "gather") == 0);
+  }();
   // taper groups of at most 8, balanced
   const int64_t k = a.tapers ? a.k : 1;
   const int64_t groups = (k + 7) / 8;
@@ -223,6 +518,11 @@ void spread_typed(const Plan& plan, const SpreadArgs& a, cudaStream_t s) {
     const int64_t kg = (k - k0 + (groups - gidx) - 1) / (groups - gidx);
     P.k0 = static_cast<int>(k0);
     P.kg = static_cast<int>(kg);
+    if (use_tc) {
+      launch_tc<Real>(P, s);
+      k0 += kg;
+      continue;
+    }
     switch (kg) {
       case 1: launch_group<Real, 1>(P, p.channels, s); break;
       case 2: launch_group<Real, 2>(P, p.channels, s); break;
