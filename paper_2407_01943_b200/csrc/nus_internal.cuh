@@ -111,6 +111,11 @@ class FftCache {
 struct FusedFft {
   bool ready = false;
   int R = 1, C = 1, RPC = 1, CW = 0, lo_bits = 0;
+  // blocked: the spread writes cell j1*C + j2 at (j2/CW)*R*CW + j1*CW + j2%CW so that every
+  // pass-A column block is contiguous (bulk-copied); lgC/lgCW are its shifts
+  bool blocked = false;
+  int lgC = 0, lgCW = 0;
+  DeviceBuffer scratch;  // pass-A output (natural layout) when blocked: [C][kpad][Mr]
   DeviceBuffer tw_r, tw_c, tw_hi, tw_lo;
 };
 

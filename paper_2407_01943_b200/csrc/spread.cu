@@ -54,10 +54,19 @@ struct SpreadParams {
   int64_t n, mr, ntiles, kpad, k_total;
   int64_t s0, s1;
   int64_t channels, nseg;
+  int blocked, lgC, lgCW;  // blocked grid layout of the fused FFT (FusedFft::blocked)
   const int32_t* seg_ranges;
   int tile, w, w2, k0, kg, x_dtype, x_complex;
   Real beta, cq[kMaxW2];
 };
+
+// Grid address of cell j: natural, or the fused FFT's blocked layout (j = j1 C + j2 stored
+// at (j2 / CW) * 4096 + j1 * CW + j2 % CW, so each pass-A column block is contiguous).
+__device__ inline int64_t cell_addr(int64_t j, int blocked, int lgC, int lgCW) {
+  if (!blocked) return j;
+  const int64_t j1 = j >> lgC, j2 = j & ((int64_t{1} << lgC) - 1);
+  return ((j2 >> lgCW) << 12) | (j1 << lgCW) | (j2 & ((int64_t{1} << lgCW) - 1));
+}
 
 template <typename Real, int KG>
 __global__ void __launch_bounds__(kThreads, 5) spread_gather_kernel(const SpreadParams<Real> P) {
@@ -166,7 +175,7 @@ __global__ void __launch_bounds__(kThreads, 5) spread_gather_kernel(const Spread
   if (cell >= P.tile) return;
 #pragma unroll
   for (int k = 0; k < KG; ++k)
-    P.grid[(c * P.kpad + P.k0 + k) * P.mr + c0 + cell] = acc[k];
+    P.grid[(c * P.kpad + P.k0 + k) * P.mr + cell_addr(c0 + cell, P.blocked, P.lgC, P.lgCW)] = acc[k];
   (void)lane;
 }
 
@@ -410,13 +419,14 @@ __global__ void __launch_bounds__(kTcWarps * 32, kTcCtasPerSm) spread_tc_kernel(
       }
     }
     if (cur.last) {
-      R2* out = P.grid + (cur.c * P.kpad + P.k0) * P.mr + cur.seg * 32;
+      R2* out = P.grid + (cur.c * P.kpad + P.k0) * P.mr;
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
+        const int64_t addr = cell_addr(cur.seg * 32 + 8 * b + g, P.blocked, P.lgC, P.lgCW);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int k = 2 * t + h;
-          if (k < P.kg) out[k * P.mr + 8 * b + g] = R2{static_cast<Real>(cr[b][h]), static_cast<Real>(ci[b][h])};
+          if (k < P.kg) out[k * P.mr + addr] = R2{static_cast<Real>(cr[b][h]), static_cast<Real>(ci[b][h])};
           cr[b][h] = 0.0;
           ci[b][h] = 0.0;
         }
@@ -484,6 +494,9 @@ void spread_typed(const Plan& plan, const SpreadArgs& a, cudaStream_t s) {
   P.seg_ranges = tb.seg_range.as<int32_t>();
   P.nseg = tb.nseg;
   P.channels = p.channels;
+  P.blocked = plan.ffft.ready && plan.ffft.blocked ? 1 : 0;
+  P.lgC = plan.ffft.lgC;
+  P.lgCW = plan.ffft.lgCW;
   P.wrap_lo = tb.wrap_lo.as<int32_t>();
   P.tapers = static_cast<const Real*>(a.tapers);
   P.x = a.x;
