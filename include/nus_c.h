@@ -171,6 +171,8 @@ int nus_mtnufft_transform_device(nus_mtnufft_t est, void* grid_dev, int64_t k0, 
  * [spread, fft, crop+power] and the number of runs recorded. */
 int nus_mtnufft_timing(nus_mtnufft_t est, int64_t max_runs);
 int nus_mtnufft_timing_read(nus_mtnufft_t est, double* stage_ms3, int64_t* runs);
+/* Names of the kernels behind the three timed stages ("spread;fft;crop+power"), ';'-separated. */
+int nus_mtnufft_stage_kernels(nus_mtnufft_t est, char* out, int64_t len);
 /* ---- inference (inference.hpp:16-48) -------------------------------------
  * Harmonic F-test (inference.cpp:132-186) on host eigencoefficients j [K][I] complex with
  * zero-frequency responses w0 [K] complex; outputs F [I], amplitude [I] complex, flags [I]

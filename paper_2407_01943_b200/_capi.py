@@ -113,6 +113,7 @@ _SIGS = {
     "nus_mtnufft_eigencoefficients": [_vp, _dp, _dp],
     "nus_mtnufft_estimate_device": [_vp, _vp, _i32, _vp, _vp, _vp],
     "nus_mtnufft_spread_device": [_vp, _vp, _i32, _i64, _i64, _vp, _i64, _vp],
+    "nus_mtnufft_stage_kernels": [_vp, ctypes.c_char_p, _i64],
     "nus_mtnufft_transform_device": [_vp, _vp, _i64, _i64, _d, _i32, _vp, _vp],
     "nus_mtnufft_bytes_model": [_vp, _i32, _dp, _dp, _dp, _dp],
     "nus_f_test": [_dp, _i64, _i64, _dp, _i64, _dp, _d, _d, _i32, _dp, _dp, ctypes.POINTER(ctypes.c_uint8)],

@@ -1,3 +1,4 @@
+#include <cstdio>
 // extern "C" boundary (include/nus_c.h).  Every entry point converts internal
 // failures into status codes + a thread-local message; nothing throws across
 // the ABI.
@@ -560,6 +561,16 @@ int nus_mtnufft_bytes_model(nus_mtnufft_t est, int32_t x_dtype, double* total, d
   return guarded([&] {
     nus::require(est != nullptr, "bytes_model: null estimator");
     nus::estimator_bytes(*est->est, x_dtype, total, spread, fft, crop);
+  });
+}
+
+int nus_mtnufft_stage_kernels(nus_mtnufft_t est, char* out, int64_t len) {
+  return guarded([&] {
+    nus::require(est != nullptr && out != nullptr && len > 0, "stage_kernels: bad arguments");
+    const char *a = nullptr, *b = nullptr;
+    nus::fft_stage_names(*est->est->plan, &a, &b);
+    const std::string names = std::string(nus::spread_kernel_name()) + ";" + a + ";" + b;
+    std::snprintf(out, static_cast<size_t>(len), "%s", names.c_str());
   });
 }
 

@@ -30,6 +30,8 @@
 
 namespace nus {
 
+bool fused_pass_b_async();
+
 namespace {
 
 constexpr int kFftThreads = 256;
@@ -695,10 +697,7 @@ void launch_rows(const Plan& plan, void* grid, int64_t k, int64_t kpad, void* j_
   const int r0 = first_radix(f.C);
   // The bulk-copy pass B is correct but measured slower than the register-loading kernel
   // on C2 (0.114 vs 0.105 ms): opt in with NUS_FFT_ASYNC_B=1.
-  static const bool async_b = [] {
-    const char* e = std::getenv("NUS_FFT_ASYNC_B");
-    return e && std::strcmp(e, "1") == 0;
-  }();
+  static const bool async_b = fused_pass_b_async();
   if (use_async(f, sizeof(T2)) && r0 == 16 && async_b) {
     const int64_t nrows = p.channels * f.R;
     const unsigned grid_x = static_cast<unsigned>(std::min<int64_t>(nrows, sm_count()));
@@ -720,6 +719,21 @@ void launch_rows(const Plan& plan, void* grid, int64_t k, int64_t kpad, void* j_
 }
 
 }  // namespace
+
+bool fused_pass_b_async() {
+  const char* e = std::getenv("NUS_FFT_ASYNC_B");
+  return e && std::strcmp(e, "1") == 0;
+}
+
+void fft_stage_names(const Plan& plan, const char** a, const char** b) {
+  if (!plan.ffft.ready) {
+    *a = "cufft (library)";
+    *b = "crop_power_kernel";
+    return;
+  }
+  *a = plan.ffft.R <= 1 ? "(none: single pass)" : plan.ffft.blocked ? "fft_cols_async_kernel" : "fft_cols_kernel";
+  *b = (plan.ffft.blocked && fused_pass_b_async()) ? "fft_rows_crop_async_kernel" : "fft_rows_crop_kernel";
+}
 
 void run_fused_pass_a(Plan& plan, void* grid, int64_t k, int64_t kpad, cudaStream_t s) {
   if (plan.ffft.R <= 1) return;

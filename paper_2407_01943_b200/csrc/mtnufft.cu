@@ -263,10 +263,14 @@ void estimator_bytes(const Estimator& est, int x_dtype, double* total, double* s
   const double b_spread = N * (8.0 + r) + K * N * r + K * Mr * c;
   const double b_fft = 2.0 * K * Mr * c;
   const double b_crop = K * I * c + I * r;
+  // per-stage figures are what each launched kernel must move: with the fused FFT the
+  // crop/power epilogue lives in pass B, which reads the K rows-transformed grids once
+  const double b_stage3 = est.plan->ffft.ready ? K * Mr * c + I * r : b_crop;
+  const double b_stage2 = est.plan->ffft.ready && est.plan->ffft.R <= 1 ? 0.0 : b_fft;
   if (spread) *spread = C * b_spread;
-  if (fft) *fft = C * b_fft;
-  if (crop) *crop = C * b_crop;
-  if (total) *total = C * (b_spread + b_fft + b_crop);
+  if (fft) *fft = C * b_stage2;
+  if (crop) *crop = C * b_stage3;
+  if (total) *total = C * (b_spread + b_fft + b_crop);  // SURVEY model (pipeline roofline)
 }
 
 }  // namespace nus

@@ -165,6 +165,8 @@ void run_crop(Plan& plan, void* grid, int64_t k, int64_t kpad, void* j_out, void
 
 // Fused two-pass FFT + crop/power (fft.cu); supported for 32 <= Mr <= 2^24.
 bool fused_fft_supported(const PlanParams& p);
+const char* spread_kernel_name();
+void fft_stage_names(const Plan& plan, const char** pass_a, const char** pass_b);
 void fused_fft_prepare(Plan& plan);
 void run_fused_pass_a(Plan& plan, void* grid, int64_t k, int64_t kpad, cudaStream_t s);
 void run_fused_pass_b(Plan& plan, void* grid, int64_t k, int64_t kpad, void* j_out, void* power, bool power_f64,

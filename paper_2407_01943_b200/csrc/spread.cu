@@ -552,6 +552,11 @@ void spread_typed(const Plan& plan, const SpreadArgs& a, cudaStream_t s) {
 
 }  // namespace
 
+const char* spread_kernel_name() {
+  const char* e = std::getenv("NUS_SPREAD");
+  return (e && std::strcmp(e, "gather") == 0) ? "spread_gather_kernel" : "spread_tc_kernel";
+}
+
 void launch_spread(const Plan& plan, const SpreadArgs& a, cudaStream_t s) {
   if (plan.p.precision == NUS_F64)
     spread_typed<double>(plan, a, s);
