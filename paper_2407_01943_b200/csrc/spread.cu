@@ -55,9 +55,14 @@ struct SpreadParams {
   int64_t s0, s1;
   int64_t channels, nseg;
   int blocked, lgC, lgCW;  // blocked grid layout of the fused FFT (FusedFft::blocked)
+  int lg_nseg;
+  const Real* taper_base;  // tapers, or a device constant 1 with zero strides
+  int64_t tstride_k, tstride_j;
   const int32_t* seg_ranges;
   int tile, w, w2, k0, kg, x_dtype, x_complex;
   Real beta, cq[kMaxW2];
+  // tensor-core staging: W_{p+2} = W_p * q_p, q_{p+2} = q_p * ve (even / odd chains)
+  double c0, c1, qe0, qo0, ve;
 };
 
 // Grid address of cell j: natural, or the fused FFT's blocked layout (j = j1 C + j2 stored
@@ -66,6 +71,12 @@ __device__ inline int64_t cell_addr(int64_t j, int blocked, int lgC, int lgCW) {
   if (!blocked) return j;
   const int64_t j1 = j >> lgC, j2 = j & ((int64_t{1} << lgC) - 1);
   return ((j2 >> lgCW) << 12) | (j1 << lgCW) | (j2 & ((int64_t{1} << lgCW) - 1));
+}
+
+__device__ inline int cell_addr32(int j, int blocked, int lgC, int lgCW) {
+  if (!blocked) return j;
+  const int j1 = j >> lgC, j2 = j & ((1 << lgC) - 1);
+  return ((j2 >> lgCW) << 12) | (j1 << lgCW) | (j2 & ((1 << lgCW) - 1));
 }
 
 template <typename Real, int KG>
@@ -192,14 +203,15 @@ __global__ void __launch_bounds__(kThreads, 5) spread_gather_kernel(const Spread
 // round n+2, so the x gather never waits on a dependent load) are in flight while round n
 // runs on the tensor cores.
 //
-// Private tables, both [row][point] with row stride kTcRows = 36 (= 4 mod 16, so the reads
-// of lane (g, t) -- row g or 8b+g, point p0+t -- and the one-lane-per-point writes are
-// bank-conflict free): WT[cell][point] = W(cell - rel_point), zero off the support and for
-// absent points, so a block needs no masking; Z[taper][point] = (re, im).  Points 32..35
-// are the zero overrun of the last 4-point step.
-constexpr int kTcWarps = 4;       // warps per CTA (each an independent worker)
-constexpr int kTcRows = 36;       // point columns per warp: 32 + overrun
-constexpr int kTcCtasPerSm = 4;
+// Private tables (row stride kTcRows = 36 = 4 mod 16): Z[taper][point] = (re, im) and
+// W[point][slot] with slot = cell mod 32, holding W(cell - rel) on the point's support only
+// (never cleared: off-support slots are masked by a range test on cell - rel).  Lane (g, t)
+// reads Z[g][p0+t] and W[p0+t][8b+g]: bank-conflict free for any rel.  rel of an absent
+// point is a far sentinel; points 32..35 absorb the last 4-point step's overrun.
+constexpr int kTcWarps = 3;       // warps per CTA (each an independent worker)
+constexpr int kTcRows = 36;       // row stride of the private tables (= 4 mod 16)
+constexpr int kTcPts = 35;        // staged point rows: 32 + the last step's overrun (p <= 34)
+constexpr int kTcCtasPerSm = 5;
 
 __device__ inline void dmma_8x8x4(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -209,64 +221,74 @@ __device__ inline void dmma_8x8x4(double& d0, double& d1, double a, double b) {
 
 // A warp's walk over its rounds: item = channel * nseg + segment; each segment visits its
 // wrapping points (part 0, segments with s0 < w2-1) then its own (part 1), 32 at a time; a
-// segment without points still yields one empty round so that its cells are written.
+// segment without points still yields one empty round so that its cells are written.  Only
+// the furthest cursor advances; the segment range it will need next is prefetched one item
+// ahead (`pre`), so no cursor step waits on a global load.
 struct TcCursor {
-  int64_t item, c, seg;
-  int part, b0, hi, nb;
-  int64_t shift;
+  int64_t item, c, seg, shift;
+  int part, b0, hi, nb, own_lo, own_hi;
   bool valid, last;
 };
 
 template <typename Real>
-__device__ inline void tc_settle(TcCursor& u, const SpreadParams<Real>& P, int64_t total) {
-  if (u.item >= total) {
+__device__ inline int4 tc_range(int64_t item, int64_t total, const SpreadParams<Real>& P) {
+  // unconditional (clamped) load: a conditional one merges with a default and the merge
+  // waits on the load; past-the-end items are never settled (valid = false)
+  return reinterpret_cast<const int4*>(P.seg_ranges)[min(item, total - 1)];
+}
+
+template <typename Real>
+__device__ inline void tc_settle(TcCursor& u, int64_t item, int4 r, const SpreadParams<Real>& P, int64_t total) {
+  u.item = item;
+  if (item >= total) {
     u.valid = false;
     u.nb = 0;
     u.last = false;
     return;
   }
   u.valid = true;
-  u.c = u.item / P.nseg;
-  u.seg = u.item - u.c * P.nseg;
-  const int4 r = reinterpret_cast<const int4*>(P.seg_ranges)[u.item];
-  const int64_t s0 = u.seg * 32;
+  u.c = item >> P.lg_nseg;  // nseg = Mr / 32 is a power of two
+  u.seg = item & (P.nseg - 1);
+  u.own_lo = r.x;
+  u.own_hi = r.y;
   if (r.z < static_cast<int>(P.n)) {
     u.part = 0;
     u.b0 = r.z;
     u.hi = static_cast<int>(P.n);
-    u.shift = s0 + P.mr;
+    u.shift = u.seg * 32 + P.mr;
   } else {
     u.part = 1;
     u.b0 = r.x;
     u.hi = r.y;
-    u.shift = s0;
+    u.shift = u.seg * 32;
   }
   u.nb = max(0, min(32, u.hi - u.b0));
-  u.last = u.b0 + 32 >= u.hi && (u.part == 1 || r.y <= r.x);
+  u.last = u.b0 + 32 >= u.hi && (u.part == 1 || u.own_hi <= u.own_lo);
 }
 
 template <typename Real>
-__device__ inline void tc_advance(TcCursor& u, const SpreadParams<Real>& P, int64_t total, int64_t stride) {
+__device__ inline void tc_advance(TcCursor& u, int4& pre, const SpreadParams<Real>& P, int64_t total,
+                                  int64_t stride) {
   if (!u.valid) return;
   if (u.b0 + 32 < u.hi) {
     u.b0 += 32;
+  } else if (u.part == 0 && u.own_hi > u.own_lo) {
+    u.part = 1;
+    u.b0 = u.own_lo;
+    u.hi = u.own_hi;
+    u.shift = u.seg * 32;
   } else {
-    const int4 r = reinterpret_cast<const int4*>(P.seg_ranges)[u.item];
-    if (u.part == 0 && r.y > r.x) {
-      u.part = 1;
-      u.b0 = r.x;
-      u.hi = r.y;
-      u.shift = u.seg * 32;
-    } else {
-      u.item += stride;
-      tc_settle(u, P, total);
-      return;
-    }
+    const int64_t next = u.item + stride;
+    const int4 r = pre;  // = range(next), loaded one item ago
+    pre = tc_range(next + stride, total, P);
+    tc_settle(u, next, r, P, total);
+    return;
   }
   u.nb = min(32, u.hi - u.b0);
   u.last = u.b0 + 32 >= u.hi && u.part == 1;
 }
 
+// x kinds (template XK): 0 f64 real, 1 f64 complex, 2 f32 real, 3 f32 complex
 template <typename Real>
 struct TcPoint {  // this lane's prefetched point of the next round: raw loads only, so the
                   // loads stay in flight until the round is staged
@@ -276,32 +298,34 @@ struct TcPoint {  // this lane's prefetched point of the next round: raw loads o
   Real w[8];
 };
 
-template <typename Real>
+// Every load is unconditional (clamped point index, clamped taper row): lanes past the
+// round's points read a real point with ti = -1, which the staging masks to x = 0; rows
+// k >= kg are read but never staged.  No lane-divergent branch, no use of loaded values.
+template <typename Real, int XK>
 __device__ inline void tc_load(TcPoint<Real>& q, int ti, const TcCursor& u, int lane, const SpreadParams<Real>& P) {
   using R2 = typename Vec2<Real>::T;
-  q.ti = -1;
-  if (!(u.valid && lane < u.nb)) return;
+  if (!u.valid || u.nb == 0) return;  // warp-uniform
+  const bool has = lane < u.nb;
+  const int j = has ? lane : u.nb - 1;
   const int64_t base = u.c * P.n;
-  const int64_t gi = base + u.b0 + lane;
-  q.ti = ti;
+  const int64_t gi = base + u.b0 + j;
+  q.ti = has ? ti : -1;
+  const int64_t xi = base + (has ? ti : 0);
   q.start = P.start[gi];
-  if (P.x_complex && P.x_dtype == 0) {
-    const ulonglong2 xv = reinterpret_cast<const ulonglong2*>(P.x)[base + ti];
+  if constexpr (XK == 1) {
+    const ulonglong2 xv = reinterpret_cast<const ulonglong2*>(P.x)[xi];
     q.xa = xv.x;
     q.xb = xv.y;
-  } else if (P.x_complex || P.x_dtype == 0) {  // f32 pair or f64 scalar: 8 bytes
-    q.xa = reinterpret_cast<const unsigned long long*>(P.x)[base + ti];
+  } else if constexpr (XK == 0 || XK == 3) {
+    q.xa = reinterpret_cast<const unsigned long long*>(P.x)[xi];
   } else {
-    q.xa = reinterpret_cast<const unsigned int*>(P.x)[base + ti];
+    q.xa = reinterpret_cast<const unsigned int*>(P.x)[xi];
   }
   q.ph = reinterpret_cast<const R2*>(P.prephase)[gi];
   q.ag = P.gauss[gi];
-  if (P.tapers) {
-    const Real* tp = P.tapers + (u.c * P.k_total + P.k0) * P.n + u.b0 + lane;
+  const Real* tp = P.taper_base + (u.c * P.k_total + P.k0) * P.tstride_k + (u.b0 + j) * P.tstride_j;
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
-      if (k < P.kg) q.w[k] = tp[k * P.n];
-  }
+  for (int k = 0; k < 8; ++k) q.w[k] = tp[min(k, P.kg - 1) * P.tstride_k];
 }
 
 template <typename Real>
@@ -309,158 +333,177 @@ __device__ inline int tc_perm(const TcCursor& u, int lane, const SpreadParams<Re
   return (u.valid && lane < u.nb) ? P.perm[u.c * P.n + u.b0 + lane] : 0;
 }
 
-template <typename Real>
+template <typename Real, int XK>
 __global__ void __launch_bounds__(kTcWarps * 32, kTcCtasPerSm) spread_tc_kernel(const SpreadParams<Real> P) {
   using R2 = typename Vec2<Real>::T;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int RS = kTcRows;
-  constexpr size_t kWarpBytes = (8 * RS) * sizeof(double2) + (32 * RS) * sizeof(double);
+  constexpr size_t kWarpBytes = (8 * RS) * sizeof(double2) + (kTcPts * RS) * sizeof(double) + RS * sizeof(int);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   double* scq = reinterpret_cast<double*>(smem_raw);     // C_p
   unsigned char* mine = smem_raw + kMaxW2 * sizeof(double) + warp * kWarpBytes;
-  double2* sz = reinterpret_cast<double2*>(mine);        // [8][RS]
-  double* sw = reinterpret_cast<double*>(sz + 8 * RS);   // [32][RS]
+  double2* sz = reinterpret_cast<double2*>(mine);        // Z [8 tapers][RS points] (rows >= KG stay 0)
+  double* sw = reinterpret_cast<double*>(sz + 8 * RS);   // W [kTcPts points][RS], slot = cell mod 32
+  int* srel = reinterpret_cast<int*>(sw + kTcPts * RS);  // rel [RS points]
 
   for (int i = threadIdx.x; i < P.w2; i += blockDim.x) scq[i] = static_cast<double>(P.cq[i]);
-  for (int i = lane; i < static_cast<int>(kWarpBytes / 16); i += 32)
+  for (int i = lane; i < static_cast<int>((kWarpBytes - RS * sizeof(int)) / 16); i += 32)
     reinterpret_cast<double2*>(mine)[i] = double2{0.0, 0.0};
+  for (int i = lane; i < RS; i += 32) srel[i] = 1 << 20;  // absent points: outside every block
   __syncthreads();
 
   const int64_t total = P.nseg * P.channels;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * kTcWarps;
+  const int64_t item0 = static_cast<int64_t>(blockIdx.x) * kTcWarps + warp;
   TcCursor cur, n1, n2;
-  cur.item = static_cast<int64_t>(blockIdx.x) * kTcWarps + warp;
-  tc_settle(cur, P, total);
+  int4 pre = tc_range(item0 + stride, total, P);
+  tc_settle(cur, item0, tc_range(item0, total, P), P, total);
   n1 = cur;
-  tc_advance(n1, P, total, stride);
+  tc_advance(n1, pre, P, total, stride);
   n2 = n1;
-  tc_advance(n2, P, total, stride);
+  tc_advance(n2, pre, P, total, stride);
   TcPoint<Real> pt;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) pt.w[k] = Real(0);
-  tc_load(pt, tc_perm(cur, lane, P), cur, lane, P);
+  pt.ti = -1;
+  tc_load<Real, XK>(pt, tc_perm(cur, lane, P), cur, lane, P);
   int perm_next = tc_perm(n1, lane, P);
 
   double cr[4][2], ci[4][2];
 #pragma unroll
   for (int b = 0; b < 4; ++b) cr[b][0] = cr[b][1] = ci[b][0] = ci[b][1] = 0.0;
 
+  const int64_t off_h0 = static_cast<int64_t>(2 * t) * P.mr, off_h1 = off_h0 + P.mr;  // tapers 2t, 2t+1
   while (cur.valid) {
-    // ---- stage round `cur`: every lane writes its point's z column and full WT column
+    // ---- stage round `cur`: lane = point; z column, rel, and the W row (support only)
     const bool has = lane < cur.nb;
-    const int rel = has ? static_cast<int>(static_cast<int64_t>(pt.start) - cur.shift) : INT32_MAX;
-#pragma unroll
-    for (int i = 0; i < 32 * RS / 64; ++i) reinterpret_cast<double2*>(sw)[lane + 32 * i] = double2{0.0, 0.0};
-    __syncwarp();
-    {
+    const bool busy = cur.nb > 0;  // empty segments only write their zeros
+    const int rel = has ? static_cast<int>(static_cast<int64_t>(pt.start) - cur.shift) : (1 << 20);
+    if (busy) {
       double xr = 0.0, xi = 0.0;
-      if (P.x_complex && P.x_dtype == 0) {
+      if constexpr (XK == 1) {
         xr = __longlong_as_double(static_cast<long long>(pt.xa));
         xi = __longlong_as_double(static_cast<long long>(pt.xb));
-      } else if (P.x_complex) {
+      } else if constexpr (XK == 3) {
         xr = __uint_as_float(static_cast<unsigned>(pt.xa));
         xi = __uint_as_float(static_cast<unsigned>(pt.xa >> 32));
-      } else if (P.x_dtype == 0) {
+      } else if constexpr (XK == 0) {
         xr = __longlong_as_double(static_cast<long long>(pt.xa));
       } else {
         xr = __uint_as_float(static_cast<unsigned>(pt.xa));
       }
-      if (!has || pt.ti < P.s0 || pt.ti >= P.s1) { xr = 0.0; xi = 0.0; }
+      if (pt.ti < P.s0 || pt.ti >= P.s1) { xr = 0.0; xi = 0.0; }  // absent lanes: ti = -1
       const double pr = static_cast<double>(pt.ph.x), pi = static_cast<double>(pt.ph.y);
-      // select, not multiply: registers of lanes without a point may hold anything (NaN)
-      const double yr = has ? xr * pr - xi * pi : 0.0, yi = has ? xr * pi + xi * pr : 0.0;
+      const double yr = xr * pr - xi * pi, yi = xr * pi + xi * pr;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const double wk = (k < P.kg && has) ? (P.tapers ? static_cast<double>(pt.w[k]) : 1.0) : 0.0;
-        sz[k * RS + lane] = double2{wk * yr, wk * yi};
+      for (int k = 0; k < 8; ++k) {  // rows k >= kg are never written: they stay zero
+        const double wk = static_cast<double>(pt.w[k]);
+        if (k < P.kg) sz[k * RS + lane] = double2{wk * yr, wk * yi};
       }
-      // WT column: W_p = A g^p C_p at cell rel + p (two interleaved recurrences)
-      if (has) {
-        const double gg = static_cast<double>(pt.ag.y), g2 = gg * gg;
-        double ae = static_cast<double>(pt.ag.x), ao = ae * gg;
+      srel[lane] = rel;
+      if (has) {  // W_p = A g^p C_p stored at slot (rel + p) mod 32 of the point's row;
+                  // C_{p+2}/C_p = e^{-4 beta (p - w + 1.5)} is a geometric chain too
+        const double gg = static_cast<double>(pt.ag.y), g2 = gg * gg, A = static_cast<double>(pt.ag.x);
+        double ae = A * P.c0, ao = A * gg * P.c1, qe = g2 * P.qe0, qo = g2 * P.qo0;
+        double* row = sw + lane * RS;
         for (int p = 0; p < P.w2; p += 2) {
-          const int c = rel + p;
-          if (static_cast<unsigned>(c) < 32u) sw[c * RS + lane] = ae * scq[p];
-          if (static_cast<unsigned>(c + 1) < 32u) sw[(c + 1) * RS + lane] = ao * scq[p + 1];
-          ae *= g2;
-          ao *= g2;
+          row[(rel + p) & 31] = ae;
+          row[(rel + p + 1) & 31] = ao;
+          ae *= qe;
+          ao *= qo;
+          qe *= P.ve;
+          qo *= P.ve;
         }
       }
     }
     __syncwarp();
     // ---- prefetch round n1 (its perm is in hand) and the perm of round n2
-    tc_load(pt, perm_next, n1, lane, P);
+    tc_load<Real, XK>(pt, perm_next, n1, lane, P);
     perm_next = tc_perm(n2, lane, P);
-    // ---- block ranges by ballot (rel ascends over the lanes), as 4-point slots
-    int slo[4], shi[4], smin = 8, smax = 0;
+    // ---- per block: its point range by ballot (rel ascends over the lanes), then exact
+    // 4-point steps on the tensor cores; a = W(cell - rel) masked to the support
+    const double* wrow = sw + t * RS + g;      // + p0*RS (points p0 + t) + 8b (slot of cell 8b + g)
+    const double2* zcol = sz + g * RS + t;     // + p0
+    const int* rcol = srel + t;
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
+    for (int b = 0; b < 4 && busy; ++b) {
       const int lo = __popc(__ballot_sync(0xffffffffu, rel < 8 * b - (P.w2 - 1)));
       const int hi = __popc(__ballot_sync(0xffffffffu, rel < 8 * b + 8));
-      slo[b] = lo >> 2;
-      shi[b] = hi > lo ? (hi + 3) >> 2 : slo[b];
-      if (shi[b] > slo[b]) {
-        smin = min(smin, slo[b]);
-        smax = max(smax, shi[b]);
-      }
-    }
-    // ---- tensor-core product: one z fragment per slot, shared by the blocks it meets
-    const double* wg = sw + g * RS + t;
-    const double2* zg = sz + g * RS + t;
-    for (int sl = smin; sl < smax; ++sl) {
-      const double2 zb = zg[4 * sl];
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        if (sl >= slo[b] && sl < shi[b]) {
-          const double a = wg[8 * b * RS + 4 * sl];
-          dmma_8x8x4(cr[b][0], cr[b][1], a, zb.x);
-          dmma_8x8x4(ci[b][0], ci[b][1], a, zb.y);
-        }
+      for (int p0 = lo; p0 < hi; p0 += 4) {  // rows up to hi + 3 <= 34: absent ones are masked
+        const int pp = 8 * b + g - rcol[p0];
+        const double wv = wrow[p0 * RS + 8 * b];
+        const double a = static_cast<unsigned>(pp) < static_cast<unsigned>(P.w2) ? wv : 0.0;
+        const double2 zb = zcol[p0];
+        dmma_8x8x4(cr[b][0], cr[b][1], a, zb.x);
+        dmma_8x8x4(ci[b][0], ci[b][1], a, zb.y);
       }
     }
     if (cur.last) {
       R2* out = P.grid + (cur.c * P.kpad + P.k0) * P.mr;
+      R2* out0 = out + off_h0;
+      R2* out1 = out + off_h1;
+      const bool k0ok = 2 * t < P.kg, k1ok = 2 * t + 1 < P.kg;
+      const int cell0 = static_cast<int>(cur.seg) * 32 + g;
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
-        const int64_t addr = cell_addr(cur.seg * 32 + 8 * b + g, P.blocked, P.lgC, P.lgCW);
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int k = 2 * t + h;
-          if (k < P.kg) out[k * P.mr + addr] = R2{static_cast<Real>(cr[b][h]), static_cast<Real>(ci[b][h])};
-          cr[b][h] = 0.0;
-          ci[b][h] = 0.0;
-        }
+        const int addr = cell_addr32(cell0 + 8 * b, P.blocked, P.lgC, P.lgCW);
+        if (k0ok) out0[addr] = R2{static_cast<Real>(cr[b][0]), static_cast<Real>(ci[b][0])};
+        if (k1ok) out1[addr] = R2{static_cast<Real>(cr[b][1]), static_cast<Real>(ci[b][1])};
+        cr[b][0] = cr[b][1] = ci[b][0] = ci[b][1] = 0.0;
       }
     }
     __syncwarp();  // private tables are restaged next
     cur = n1;
     n1 = n2;
-    tc_advance(n2, P, total, stride);
+    tc_advance(n2, pre, P, total, stride);
   }
 }
 
-template <typename Real>
+template <typename Real, int XK>
 void launch_tc(const SpreadParams<Real>& P, cudaStream_t s) {
-  const size_t warp_bytes = (8 * kTcRows) * sizeof(double2) + (32 * kTcRows) * sizeof(double);
+  const size_t warp_bytes =
+      (8 * kTcRows) * sizeof(double2) + (kTcPts * kTcRows) * sizeof(double) + kTcRows * sizeof(int);
   const size_t smem = kMaxW2 * sizeof(double) + kTcWarps * warp_bytes;
   static int blocks_per_sm = 0, sms = 0;
-  static size_t smem_cfg = 0;
-  if (smem_cfg != smem) {
-    NUS_CUDA(cudaFuncSetAttribute(spread_tc_kernel<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (blocks_per_sm == 0) {
+    NUS_CUDA(cudaFuncSetAttribute(spread_tc_kernel<Real, XK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
     int dev = 0;
     NUS_CUDA(cudaGetDevice(&dev));
     NUS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    NUS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, spread_tc_kernel<Real>, kTcWarps * 32,
-                                                           smem));
-    smem_cfg = smem;
+    NUS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, spread_tc_kernel<Real, XK>,
+                                                           kTcWarps * 32, smem));
+    require(blocks_per_sm > 0, "spread: tensor-core kernel does not fit on an SM");
   }
-  require(blocks_per_sm > 0, "spread: tensor-core kernel does not fit on an SM");
   const int64_t warps = P.nseg * P.channels;
   const int64_t grid = std::min<int64_t>((warps + kTcWarps - 1) / kTcWarps, static_cast<int64_t>(blocks_per_sm) * sms);
-  spread_tc_kernel<Real><<<static_cast<unsigned>(grid), kTcWarps * 32, smem, s>>>(P);
+  spread_tc_kernel<Real, XK><<<static_cast<unsigned>(grid), kTcWarps * 32, smem, s>>>(P);
   note_launch();
   check_launch("spread_tc_kernel");
+}
+
+__device__ double g_one_f64 = 1.0;
+__device__ float g_one_f32 = 1.0f;
+
+template <typename Real>
+void launch_tc_x(SpreadParams<Real> P, cudaStream_t s) {
+  if (P.tapers) {
+    P.taper_base = P.tapers;
+    P.tstride_k = P.n;
+    P.tstride_j = 1;
+  } else {  // untapered: every weight reads one device constant 1
+    void* one = nullptr;
+    if constexpr (sizeof(Real) == 8) NUS_CUDA(cudaGetSymbolAddress(&one, g_one_f64));
+    else NUS_CUDA(cudaGetSymbolAddress(&one, g_one_f32));
+    P.taper_base = static_cast<const Real*>(one);
+    P.tstride_k = 0;
+    P.tstride_j = 0;
+  }
+  const int xk = P.x_dtype == 0 ? (P.x_complex ? 1 : 0) : (P.x_complex ? 3 : 2);
+  switch (xk) {
+    case 0: launch_tc<Real, 0>(P, s); break;
+    case 1: launch_tc<Real, 1>(P, s); break;
+    case 2: launch_tc<Real, 2>(P, s); break;
+    default: launch_tc<Real, 3>(P, s); break;
+  }
 }
 
 template <typename Real, int KG>
@@ -493,6 +536,8 @@ void spread_typed(const Plan& plan, const SpreadArgs& a, cudaStream_t s) {
   P.ranges = tb.tile_range.as<int32_t>();
   P.seg_ranges = tb.seg_range.as<int32_t>();
   P.nseg = tb.nseg;
+  P.lg_nseg = 0;
+  while ((int64_t{1} << P.lg_nseg) < tb.nseg) ++P.lg_nseg;
   P.channels = p.channels;
   P.blocked = plan.ffft.ready && plan.ffft.blocked ? 1 : 0;
   P.lgC = plan.ffft.lgC;
@@ -518,6 +563,17 @@ void spread_typed(const Plan& plan, const SpreadArgs& a, cudaStream_t s) {
     const double qc = static_cast<double>(q) - (static_cast<double>(p.w) - 0.5);
     P.cq[q] = static_cast<Real>(std::exp(-p.beta * qc * qc));
   }
+  {
+    auto cexp = [&](double q) {
+      const double qc = q - (static_cast<double>(p.w) - 0.5);
+      return std::exp(-p.beta * qc * qc);
+    };
+    P.c0 = cexp(0.0);
+    P.c1 = cexp(1.0);
+    P.qe0 = std::exp(-4.0 * p.beta * (1.5 - static_cast<double>(p.w)));  // C_2 / C_0
+    P.qo0 = std::exp(-4.0 * p.beta * (2.5 - static_cast<double>(p.w)));  // C_3 / C_1
+    P.ve = std::exp(-8.0 * p.beta);
+  }
   // NUS_SPREAD=gather selects the CUDA-core broadcast gather (kept for comparison)
   static const bool use_tc = [] {
     const char* e = std::getenv("NUS_SPREAD");
@@ -532,7 +588,7 @@ void spread_typed(const Plan& plan, const SpreadArgs& a, cudaStream_t s) {
     P.k0 = static_cast<int>(k0);
     P.kg = static_cast<int>(kg);
     if (use_tc) {
-      launch_tc<Real>(P, s);
+      launch_tc_x<Real>(P, s);
       k0 += kg;
       continue;
     }
