@@ -141,6 +141,8 @@ __device__ inline void fft16_regs(T2 (&v)[16], T2* buf, int lgL, int lgNfft, int
   constexpr int B0 = 16 / R0;
   constexpr int lgR0 = R0 == 16 ? 4 : R0 == 8 ? 3 : R0 == 4 ? 2 : 1;
   const int nfm = (1 << lgNfft) - 1;
+  // the first radix-16 stage's twiddle, loaded before stage 0 so that its latency hides
+  T2 w_next = tw[(((tid >> lgNfft) & ((1 << (lgL - 4)) - 1)) & ((1 << lgR0) - 1)) << (lgL - lgR0 - 4)];
   // ---- stage 0 (registers -> shared)
   {
     const int lgNb = lgL - lgR0;
@@ -161,10 +163,12 @@ __device__ inline void fft16_regs(T2 (&v)[16], T2* buf, int lgL, int lgNfft, int
   const int u = tid;
   const int f = u & nfm, j = (u >> lgNfft) & ((1 << lgNb) - 1);
   const int in0 = f * fs + j * es;
+  // each later stage's twiddle is loaded one stage ahead (its latency hides behind a stage)
   for (int lgNs = lgR0; lgNs < lgL; lgNs += 4) {
     const int Ns = 1 << lgNs;
     const int jm = j & (Ns - 1);
-    const T2 w1 = tw[jm << (lgL - lgNs - 4)];
+    const T2 w1 = w_next;
+    if (lgNs + 4 < lgL) w_next = tw[(j & ((Ns << 4) - 1)) << (lgL - lgNs - 8)];
     T2 wq = w1;
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
@@ -203,6 +207,28 @@ __device__ inline void stage0_index(int slot, int lgL, int lgNfft, int& f, int& 
   e = j + (q << lgNb);
 }
 
+// Output placement of fft16_regs' last (register-resident) radix-16 stage, known before the
+// transform: FFT f = tid mod Nfft, outputs out0 + q*st with out0 = j, st = L/16.
+__device__ inline void last_stage_out(int tid, int lgL, int lgNfft, int& f, int& out0, int& st) {
+  f = tid & ((1 << lgNfft) - 1);
+  out0 = (tid >> lgNfft) & ((1 << (lgL - 4)) - 1);
+  st = 1 << (lgL - 4);
+}
+
+// Inter-pass twiddle pair for w_Mr^{j2 (out0 + q st)}: base w^{j2 out0} and step w^{j2 st}, each
+// a product of the two-level table entries (hi, lo).
+template <typename T2>
+struct PassATwiddles {
+  T2 b_hi, b_lo, s_hi, s_lo;
+};
+template <typename T2>
+__device__ inline PassATwiddles<T2> pass_a_twiddles(int64_t j2, int out0, int st, int64_t mr, int lo_bits,
+                                                    const T2* __restrict__ tw_hi, const T2* __restrict__ tw_lo) {
+  const int64_t lo_mask = (int64_t{1} << lo_bits) - 1;
+  const int64_t a0 = (j2 * out0) & (mr - 1), as = (j2 * st) & (mr - 1);
+  return PassATwiddles<T2>{tw_hi[a0 >> lo_bits], tw_lo[a0 & lo_mask], tw_hi[as >> lo_bits], tw_lo[as & lo_mask]};
+}
+
 // ---- pass A ----------------------------------------------------------------------------
 
 template <typename Real, int R0>
@@ -217,7 +243,9 @@ __global__ void __launch_bounds__(kFftThreads, 2) fft_cols_kernel(
   const int j2_0 = blockIdx.x * CW;
   const int64_t ch = blockIdx.y;
   const int lgR = __ffs(R) - 1, lgCW = __ffs(CW) - 1;
-  const int64_t lo_mask = (int64_t{1} << lo_bits) - 1;
+  int fl, out0l, stl;
+  last_stage_out(threadIdx.x, lgR, lgCW, fl, out0l, stl);
+  const PassATwiddles<T2> tw2 = pass_a_twiddles(j2_0 + fl, out0l, stl, mr, lo_bits, tw_hi, tw_lo);
   for (int kk = 0; kk < rows_per_ch; ++kk) {
     T2* g = grid + (ch * kpad + kk) * row_stride;
     T2 v[16];
@@ -230,12 +258,13 @@ __global__ void __launch_bounds__(kFftThreads, 2) fft_cols_kernel(
     int f, out0, step;
     fft16_regs<R0, false>(v, buf, lgR, lgCW, CW, 1, tw_r, f, out0, step);
     const int64_t j2 = j2_0 + f;
+    T2 w = cmul(tw2.b_hi, tw2.b_lo);  // inter-pass twiddle w_Mr^{j2 k1}, k1 = out0 + q step
+    const T2 wstep = cmul(tw2.s_hi, tw2.s_lo);
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
       const int k1 = out0 + q * step;
-      const int64_t a = (j2 * k1) & (mr - 1);  // inter-pass twiddle w_Mr^{j2 k1}
-      const T2 w = cmul(tw_hi[a >> lo_bits], tw_lo[a & lo_mask]);
       g[static_cast<int64_t>(k1) * C + j2] = cmul(v[q], w);
+      if (q < 15) w = cmul(w, wstep);
     }
     __syncthreads();  // buf reused by the next taper
   }
@@ -382,7 +411,6 @@ __global__ void __launch_bounds__(kFftThreads * kGroups, 1) fft_cols_async_kerne
   uint64_t* bars = reinterpret_cast<uint64_t*>(bufs + kBufs * kFftElems);
   const int64_t nblk = C / CW;
   const int lgR = __ffs(R) - 1, lgCW = __ffs(CW) - 1;
-  const int64_t lo_mask = (int64_t{1} << lo_bits) - 1;
   const int grp = threadIdx.x / kFftThreads, gt = threadIdx.x % kFftThreads;
   const int64_t step = gridDim.x;
   const int64_t nmine = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / step + 1 : 0;
@@ -398,6 +426,14 @@ __global__ void __launch_bounds__(kFftThreads * kGroups, 1) fft_cols_async_kerne
     const int b = static_cast<int>(i % kBufs);
     T2* const buf = bufs + b * kFftElems;
     const int64_t t = blockIdx.x + i * step;
+    // fp32: the base/step twiddles are loaded before the FFT (they land during it); fp64 has
+    // no registers to spare across the transform and loads them after it (one L1 latency)
+    PassATwiddles<T2> tw2;
+    if constexpr (sizeof(Real) == 4) {
+      int fl, out0l, stl;
+      last_stage_out(gt, lgR, lgCW, fl, out0l, stl);
+      tw2 = pass_a_twiddles((t % nblk) * CW + fl, out0l, stl, mr, lo_bits, tw_hi, tw_lo);
+    }
     mbar_wait(&bars[b], static_cast<uint32_t>((i / kBufs) & 1));
     T2 v[16];
 #pragma unroll
@@ -413,12 +449,16 @@ __global__ void __launch_bounds__(kFftThreads * kGroups, 1) fft_cols_async_kerne
     const int64_t ch = ck / k, kk = ck - ch * k;
     T2* g = out + (ch * kpad + kk) * mr;  // out of place: the blocked input is still being read
     const int64_t j2 = blk * CW + f;
+    if constexpr (sizeof(Real) == 8) tw2 = pass_a_twiddles(j2, out0, st, mr, lo_bits, tw_hi, tw_lo);
+    // inter-pass twiddles w_Mr^{j2 k1}, k1 = out0 + q st: w_base * w_step^q (base and step were
+    // loaded from the two-level table before the FFT; 15 complex products instead of 30 loads)
+    T2 w = cmul(tw2.b_hi, tw2.b_lo);
+    const T2 wstep = cmul(tw2.s_hi, tw2.s_lo);
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
       const int k1 = out0 + q * st;
-      const int64_t a = (j2 * k1) & (mr - 1);  // inter-pass twiddle w_Mr^{j2 k1}
-      const T2 w = cmul(tw_hi[a >> lo_bits], tw_lo[a & lo_mask]);
       g[static_cast<int64_t>(k1) * C + j2] = cmul(v[q], w);  // natural row-major layout for pass B
+      if (q < 15) w = cmul(w, wstep);
     }
     group_bar(1 + grp);  // buf consumed: refill it with tile i + 3
     if (gt == 0 && i + kBufs < nmine)
