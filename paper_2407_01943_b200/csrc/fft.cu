@@ -390,6 +390,37 @@ __device__ inline void issue_tile(T2* dst, const T2* src, int count, uint64_t* b
 constexpr int kGroups = 2;
 constexpr int kBufs = 3;
 
+// Pass-A tile load restricted to the occupied rows [row_lo, row_lo + row_cnt) (cyclic): one
+// or two contiguous runs of the tile (row j1 at offset j1 * CW); the rest is zero-filled at
+// stage 0.
+// The other rows are copied from a zero buffer (L2-resident), so the tile is complete and
+// stage 0 reads it unconditionally.
+template <typename T2>
+__device__ inline void issue_cols_tile(T2* dst, const T2* src, const T2* zeros, int R, int CW, int row_lo,
+                                       int row_cnt, uint64_t* bar) {
+  const uint32_t row_bytes = static_cast<uint32_t>(CW * sizeof(T2));
+  fence_proxy_async();
+  mbar_expect_tx(bar, row_bytes * static_cast<uint32_t>(R));
+  constexpr uint32_t kChunk = 16384;
+  auto copy = [&](int r0, int rows, bool zero) {
+    const uint32_t bytes = row_bytes * static_cast<uint32_t>(rows);
+    unsigned char* d = reinterpret_cast<unsigned char*>(dst + r0 * CW);
+    const unsigned char* s = reinterpret_cast<const unsigned char*>(zero ? zeros : src + r0 * CW);
+    for (uint32_t o = 0; o < bytes; o += kChunk)
+      bulk_g2s(d + o, zero ? s : s + o, min(kChunk, bytes - o), bar);
+  };
+  const int end = row_lo + row_cnt;  // occupied: [row_lo, end) mod R
+  if (end <= R) {
+    if (row_lo > 0) copy(0, row_lo, true);
+    copy(row_lo, row_cnt, false);
+    if (end < R) copy(end, R - end, true);
+  } else {
+    copy(0, end - R, false);
+    copy(end - R, row_lo - (end - R), true);
+    copy(row_lo, R - row_lo, false);
+  }
+}
+
 // pass A: tile t = ((ch * k) + kk) * nblk + blk is the contiguous column block blk of the
 // blocked grid layout (spread.cu writes cell j1 C + j2 at blk*R*CW + j1*CW + (j2 % CW)).
 template <typename T2>
@@ -404,7 +435,8 @@ __global__ void __launch_bounds__(kFftThreads * kGroups, 1) fft_cols_async_kerne
     const typename C2<Real>::T* __restrict__ grid, typename C2<Real>::T* __restrict__ out, int64_t mr, int R, int C,
     int CW, int64_t ntiles, int k, int kpad,
     const typename C2<Real>::T* __restrict__ tw_r, const typename C2<Real>::T* __restrict__ tw_hi,
-    const typename C2<Real>::T* __restrict__ tw_lo, int lo_bits) {
+    const typename C2<Real>::T* __restrict__ tw_lo, int lo_bits, int row_lo, int row_cnt,
+    const typename C2<Real>::T* __restrict__ zeros) {
   using T2 = typename C2<Real>::T;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T2* const bufs = reinterpret_cast<T2*>(smem_raw);
@@ -418,8 +450,8 @@ __global__ void __launch_bounds__(kFftThreads * kGroups, 1) fft_cols_async_kerne
     for (int b = 0; b < kBufs; ++b) mbar_init(&bars[b], 1);
     fence_mbar_init();
     for (int b = 0; b < kBufs && b < nmine; ++b)
-      issue_tile(bufs + b * kFftElems, cols_tile_src(grid, blockIdx.x + b * step, nblk, k, kpad, mr), kFftElems,
-                 &bars[b]);
+      issue_cols_tile(bufs + b * kFftElems, cols_tile_src(grid, blockIdx.x + b * step, nblk, k, kpad, mr), zeros, R,
+                      CW, row_lo, row_cnt, &bars[b]);
   }
   __syncthreads();
   for (int64_t i = grp; i < nmine; i += kGroups) {
@@ -462,7 +494,8 @@ __global__ void __launch_bounds__(kFftThreads * kGroups, 1) fft_cols_async_kerne
     }
     group_bar(1 + grp);  // buf consumed: refill it with tile i + 3
     if (gt == 0 && i + kBufs < nmine)
-      issue_tile(buf, cols_tile_src(grid, blockIdx.x + (i + kBufs) * step, nblk, k, kpad, mr), kFftElems, &bars[b]);
+      issue_cols_tile(buf, cols_tile_src(grid, blockIdx.x + (i + kBufs) * step, nblk, k, kpad, mr), zeros, R, CW,
+                      row_lo, row_cnt, &bars[b]);
   }
 }
 
@@ -619,6 +652,8 @@ void fused_fft_prepare(Plan& plan) {
   const bool f64 = p.precision == NUS_F64;
   const size_t cb = f64 ? sizeof(double2) : sizeof(float2);
   const int64_t hi_count = (p.mr >> f.lo_bits), lo_count = int64_t{1} << f.lo_bits;
+  f.zeros.alloc(16384);  // bulk-copy source for the unoccupied rows of pass-A tiles
+  NUS_CUDA(cudaMemset(f.zeros.ptr, 0, f.zeros.bytes));
   f.tw_r.alloc(std::max(f.R, 2) * cb);
   f.tw_c.alloc(f.C * cb);
   f.tw_hi.alloc(hi_count * cb);
@@ -705,7 +740,8 @@ void launch_cols(const Plan& plan, void* grid, void* scratch, int64_t k, int64_t
 #define NUS_COLS_ASYNC(R0)                                                                                   \
   fft_cols_async_kernel<Real, R0><<<grid_x, kFftThreads * kGroups, smem, s>>>(g, out, p.mr, f.R, f.C, f.CW, ntiles, \
                                                                     static_cast<int>(k), static_cast<int>(kpad), \
-                                                                    tr, th, tl, f.lo_bits)
+                                                                    tr, th, tl, f.lo_bits, f.row_lo, f.row_cnt, \
+                                                                    f.zeros.as<T2>())
     if (r0 == 16) NUS_COLS_ASYNC(16);
     else if (r0 == 8) NUS_COLS_ASYNC(8);
     else if (r0 == 4) NUS_COLS_ASYNC(4);

@@ -116,7 +116,12 @@ struct FusedFft {
   bool blocked = false;
   int lgC = 0, lgCW = 0;
   DeviceBuffer scratch;  // pass-A output (natural layout) when blocked: [C][kpad][Mr]
+  // Occupied rows (blocked only): every cell any point's support touches lies in rows
+  // j1 in [row_lo, row_lo + row_cnt) (cyclic, union over channels).  The spread writes only
+  // those rows and pass A loads only them; the other rows are exact zeros of the grid.
+  int row_lo = 0, row_cnt = 1;
   DeviceBuffer tw_r, tw_c, tw_hi, tw_lo;
+  DeviceBuffer zeros;  // 16 KB of zeros (bulk-copy source)
 };
 
 struct Plan {

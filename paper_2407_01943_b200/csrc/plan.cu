@@ -240,6 +240,16 @@ __global__ void seg_ranges_kernel(const int32_t* __restrict__ start, int64_t n, 
   ranges[4 * g + 3] = 0;
 }
 
+// Rows j1 = cell >> lgC touched by a point's support [start, start + w2) mod Mr (<= 2 rows).
+__global__ void row_occupancy_kernel(const int32_t* __restrict__ start, int64_t total, int w2, int64_t mr,
+                                     int lgC, uint8_t* __restrict__ occ) {
+  const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (g >= total) return;
+  const int64_t s = start[g];
+  occ[s >> lgC] = 1;
+  occ[((s + w2 - 1) & (mr - 1)) >> lgC] = 1;
+}
+
 template <typename Real>
 __global__ void deconv_kernel(int64_t nc, int64_t mode_offset, double tau, double norm,
                               Real* __restrict__ out) {
@@ -346,6 +356,36 @@ void plan_build_tables(Plan& plan, cudaStream_t st) {
   NUS_CUDA(cudaStreamSynchronize(st));
   const char* fft_env = std::getenv("NUS_FFT");
   if (!(fft_env && std::strcmp(fft_env, "cufft") == 0)) fused_fft_prepare(plan);
+  FusedFft& ff = plan.ffft;
+  ff.row_lo = 0;
+  ff.row_cnt = ff.R;
+  if (ff.ready && ff.blocked && p.n > 0) {
+    // minimal cyclic row interval covering every occupied row: complement of the largest gap
+    DeviceBuffer occ(static_cast<size_t>(ff.R));
+    NUS_CUDA(cudaMemsetAsync(occ.ptr, 0, occ.bytes, st));
+    const int64_t total = p.channels * p.n;
+    row_occupancy_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(
+        tb.start.as<int32_t>(), total, 2 * p.w, p.mr, ff.lgC, occ.as<uint8_t>());
+    note_launch();
+    check_launch("row_occupancy_kernel");
+    std::vector<uint8_t> h(ff.R);
+    NUS_CUDA(cudaMemcpyAsync(h.data(), occ.ptr, ff.R, cudaMemcpyDeviceToHost, st));
+    NUS_CUDA(cudaStreamSynchronize(st));
+    int best_len = 0, best_end = 0;  // largest run of empty rows, cyclic
+    for (int start_row = 0; start_row < ff.R; ++start_row) {
+      if (h[start_row] || h[(start_row + ff.R - 1) % ff.R] == 0) continue;  // runs start after an occupied row
+      int len = 0;
+      while (len < ff.R && h[(start_row + len) % ff.R] == 0) ++len;
+      if (len > best_len) {
+        best_len = len;
+        best_end = (start_row + len) % ff.R;
+      }
+    }
+    if (best_len > 0 && best_len < ff.R) {
+      ff.row_lo = best_end;
+      ff.row_cnt = ff.R - best_len;
+    }
+  }
 }
 
 std::unique_ptr<Plan> plan_create(const double* times, int64_t channels, int64_t n,

@@ -56,6 +56,10 @@ struct SpreadParams {
   int64_t channels, nseg;
   int blocked, lgC, lgCW;  // blocked grid layout of the fused FFT (FusedFft::blocked)
   int lg_nseg;
+  // items = channels * nseg_used segments: rows (of 2^lg_spr segments) row_lo .. row_lo+row_cnt-1
+  // (cyclic mod nrows) of each channel; other rows are never written (FusedFft::row_lo)
+  int lg_spr, row_lo, nrows;
+  int64_t nseg_used;
   const Real* taper_base;  // tapers, or a device constant 1 with zero strides
   int64_t tstride_k, tstride_j;
   const int32_t* seg_ranges;
@@ -230,11 +234,22 @@ struct TcCursor {
   bool valid, last;
 };
 
+// item -> (channel, segment): the channel's segments of rows row_lo .. row_lo + row_cnt - 1
+template <typename Real>
+__device__ inline void tc_item(int64_t item, const SpreadParams<Real>& P, int64_t& c, int64_t& seg) {
+  c = item / P.nseg_used;
+  const int64_t s = item - c * P.nseg_used;
+  const int64_t row = ((s >> P.lg_spr) + P.row_lo) & (P.nrows - 1);
+  seg = (row << P.lg_spr) | (s & ((int64_t{1} << P.lg_spr) - 1));
+}
+
 template <typename Real>
 __device__ inline int4 tc_range(int64_t item, int64_t total, const SpreadParams<Real>& P) {
   // unconditional (clamped) load: a conditional one merges with a default and the merge
   // waits on the load; past-the-end items are never settled (valid = false)
-  return reinterpret_cast<const int4*>(P.seg_ranges)[min(item, total - 1)];
+  int64_t c, seg;
+  tc_item(min(item, total - 1), P, c, seg);
+  return reinterpret_cast<const int4*>(P.seg_ranges)[c * P.nseg + seg];
 }
 
 template <typename Real>
@@ -247,8 +262,7 @@ __device__ inline void tc_settle(TcCursor& u, int64_t item, int4 r, const Spread
     return;
   }
   u.valid = true;
-  u.c = item >> P.lg_nseg;  // nseg = Mr / 32 is a power of two
-  u.seg = item & (P.nseg - 1);
+  tc_item(item, P, u.c, u.seg);
   u.own_lo = r.x;
   u.own_hi = r.y;
   if (r.z < static_cast<int>(P.n)) {
@@ -352,7 +366,7 @@ __global__ void __launch_bounds__(kTcWarps * 32, kTcCtasPerSm) spread_tc_kernel(
   for (int i = lane; i < RS; i += 32) srel[i] = 1 << 20;  // absent points: outside every block
   __syncthreads();
 
-  const int64_t total = P.nseg * P.channels;
+  const int64_t total = P.nseg_used * P.channels;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * kTcWarps;
   const int64_t item0 = static_cast<int64_t>(blockIdx.x) * kTcWarps + warp;
   TcCursor cur, n1, n2;
@@ -473,7 +487,7 @@ void launch_tc(const SpreadParams<Real>& P, cudaStream_t s) {
                                                            kTcWarps * 32, smem));
     require(blocks_per_sm > 0, "spread: tensor-core kernel does not fit on an SM");
   }
-  const int64_t warps = P.nseg * P.channels;
+  const int64_t warps = P.nseg_used * P.channels;
   const int64_t grid = std::min<int64_t>((warps + kTcWarps - 1) / kTcWarps, static_cast<int64_t>(blocks_per_sm) * sms);
   spread_tc_kernel<Real, XK><<<static_cast<unsigned>(grid), kTcWarps * 32, smem, s>>>(P);
   note_launch();
@@ -540,6 +554,17 @@ void spread_typed(const Plan& plan, const SpreadArgs& a, cudaStream_t s) {
   while ((int64_t{1} << P.lg_nseg) < tb.nseg) ++P.lg_nseg;
   P.channels = p.channels;
   P.blocked = plan.ffft.ready && plan.ffft.blocked ? 1 : 0;
+  if (P.blocked) {  // only the occupied rows of pass A (the others stay unwritten zeros)
+    P.lg_spr = plan.ffft.lgC - 5;
+    P.row_lo = plan.ffft.row_lo;
+    P.nrows = plan.ffft.R;
+    P.nseg_used = static_cast<int64_t>(plan.ffft.row_cnt) << P.lg_spr;
+  } else {
+    P.lg_spr = P.lg_nseg;
+    P.row_lo = 0;
+    P.nrows = 1;
+    P.nseg_used = tb.nseg;
+  }
   P.lgC = plan.ffft.lgC;
   P.lgCW = plan.ffft.lgCW;
   P.wrap_lo = tb.wrap_lo.as<int32_t>();
