@@ -11,7 +11,7 @@ NVFLAGS  := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC \
             --expt-relaxed-constexpr -Iinclude -I$(SRC) -Xptxas -warn-spills
 HDRS     := include/nus_c.h $(SRC)/nus_internal.cuh $(SRC)/nus_estimator.cuh
 
-.PHONY: all lib cpp oracle reftests clean
+.PHONY: all lib cpp oracle reftests iocheck clean
 
 all: lib cpp oracle
 
@@ -30,6 +30,12 @@ build/host/%.o: $(SRC)/host/%.cpp $(wildcard include/nuspectral/*.hpp) include/n
 
 $(LIBDIR)/libnuspectral_b200.so: $(HOST_OBJS) $(LIBDIR)/libnus_b200.so
 	$(CXX) -shared -o $@ $(HOST_OBJS) -L$(LIBDIR) -lnus_b200 -Wl,-rpath,'$$ORIGIN'
+
+# test adapter: C-ABI over the drop-in I/O (tests/test_io.py), host code only
+iocheck: tests/io/libiocheck.so
+tests/io/libiocheck.so: tests/io/io_capi.cpp $(LIBDIR)/libnuspectral_b200.so include/nuspectral/io.hpp
+	$(CXX) $(CXXFLAGS) -shared -o $@ $< -L$(LIBDIR) -lnuspectral_b200 -lnus_b200 \
+	    -Wl,-rpath,'$$ORIGIN/../../$(LIBDIR)'
 
 # The reference's own doctest files compiled UNCHANGED against the drop-in headers
 # (test infrastructure; needs /root/reference, outputs travel in oracle/_ref/dropin).
