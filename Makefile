@@ -5,7 +5,7 @@ ARCH     := -gencode arch=compute_100a,code=sm_100a
 PKG      := paper_2407_01943_b200
 SRC      := $(PKG)/csrc
 LIBDIR   := $(PKG)/lib
-CU_SRCS  := $(SRC)/plan.cu $(SRC)/spread.cu $(SRC)/fft.cu $(SRC)/transform.cu $(SRC)/tapers.cu $(SRC)/mtnufft.cu $(SRC)/ftest.cu $(SRC)/capi.cu
+CU_SRCS  := $(SRC)/plan.cu $(SRC)/spread.cu $(SRC)/fft.cu $(SRC)/transform.cu $(SRC)/tapers.cu $(SRC)/mtnufft.cu $(SRC)/ftest.cu $(SRC)/gep.cu $(SRC)/capi.cu
 CU_OBJS  := $(patsubst $(SRC)/%.cu,build/cu/%.o,$(CU_SRCS))
 NVFLAGS  := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC \
             --expt-relaxed-constexpr -Iinclude -I$(SRC) -Xptxas -warn-spills
@@ -41,7 +41,7 @@ tests/io/libiocheck.so: tests/io/io_capi.cpp $(LIBDIR)/libnuspectral_b200.so inc
 # (test infrastructure; needs /root/reference, outputs travel in oracle/_ref/dropin).
 REF       ?= /root/reference/proj
 DROPIN    := oracle/_ref/dropin
-REFTESTS  := test_nufft test_fft test_grid
+REFTESTS  := test_nufft test_fft test_grid test_eig
 REFT_FLAGS := -std=gnu++20 -O2 -Iinclude -Itests/dropin -I$(REF)/include -I$(REF)/tests
 reftests: $(addprefix $(DROPIN)/,$(REFTESTS))
 
@@ -64,7 +64,7 @@ build/cu/%.o: $(SRC)/%.cu $(HDRS)
 
 $(LIBDIR)/libnus_b200.so: $(CU_OBJS)
 	@mkdir -p $(LIBDIR)
-	$(NVCC) $(ARCH) -shared -o $@ $^ -lcufft -Xlinker -rpath -Xlinker /usr/local/cuda/lib64
+	$(NVCC) $(ARCH) -shared -o $@ $^ -lcufft -lcusolver -lcublas -Xlinker -rpath -Xlinker /usr/local/cuda/lib64
 
 oracle:
 	$(MAKE) -s -C oracle all

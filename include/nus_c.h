@@ -46,7 +46,9 @@ enum nus_status {
   NUS_ERR_CUDA = 6,             /* CUDA / cuFFT runtime failure */
   NUS_ERR_OUT_OF_MEMORY = 7,
   NUS_ERR_NO_DEVICE = 8,
-  NUS_ERR_DEGENERATE_TAPERS = 9 /* nuspectral::DegenerateTapers */
+  NUS_ERR_DEGENERATE_TAPERS = 9, /* nuspectral::DegenerateTapers */
+  NUS_ERR_CONDITIONING = 10,     /* nuspectral::ConditioningError (eig.cpp:497-499) */
+  NUS_ERR_SPECTRAL_RANGE = 11    /* nuspectral::SpectralRangeError (eig.cpp:542-545) */
 };
 
 enum nus_path_policy { NUS_AUTO_SELECT = 0, NUS_FORCE_FAST = 1, NUS_FORCE_DIRECT = 2 };
@@ -104,6 +106,26 @@ int nus_fft_inplace(double* data_host, int64_t n, int32_t inverse, int32_t devic
 /* Dense R(B) (n x n row-major) filled on the device (signal_band_kernel, kernels.cpp:100-115). */
 int nus_signal_band_matrix(const double* times, int64_t n, double f_max, int32_t device,
                            double* out_host);
+
+/* ---- MTNUFFT0: exact nominal-band tapers ----------------
+ * Generalized Hermitian eigenproblem A w = lambda M w (eig.cpp:612-659) on the device:
+ * Cholesky of M + ridge * trace(M)/n * I (ridge_first, then ridge_retry; else
+ * NUS_ERR_CONDITIONING), C = L^-1 A L^-T, the k largest eigenpairs, values descending
+ * clamped into [0, 1] (NUS_ERR_SPECTRAL_RANGE beyond 1e-6), vectors w = L^-T y normalised to
+ * w^H M w = 1 with the canonical phase (largest |w_i| real positive), residuals
+ * ||A w - lambda M w|| / (||A||_F ||w||).  A: n x n row-major (a_im null when real),
+ * M: n x n row-major real symmetric; vectors: [k][n] complex. */
+int nus_generalized_eigen(const double* a_re, const double* a_im, const double* m, int64_t n, int64_t k,
+                          double ridge_first, double ridge_retry, int32_t want_vectors, int32_t device,
+                          double* values, double* vectors, double* residuals);
+/* Dense analysis-band kernel R(A) (n x n row-major; im_out null for a band centred at 0),
+ * filled on the device (analysis_band_kernel, kernels.cpp:117-153). */
+int nus_band_matrix(const double* times, int64_t n, double f_w, double f_center, int32_t device, double* re_out,
+                    double* im_out);
+/* gpss_exact (tapers.cpp:118-144): R(B) and R(A) (band f_center +- f_w) built on the device,
+ * the GEP above, each vector scaled to w^H R(B) w = 2 f_w.  w_out [k][n] complex. */
+int nus_gpss_exact(const double* times, int64_t n, double f_max, double f_center, double f_w, int64_t k,
+                   double ridge_first, double ridge_retry, int32_t device, double* w_out, double* concentrations);
 
 /* ---- tapers (tapers.hpp) -------------------------------------------------- */
 /* Top-k eigenpairs of the commuting tridiagonal (tapers.cpp:40-52); vectors K x n unit norm,

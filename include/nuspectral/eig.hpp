@@ -25,6 +25,23 @@ struct EigenPairs {
 
 EigenPairs tridiagonal_eigen(const std::vector<double>& diag, const std::vector<double>& offdiag,
                              std::size_t k_top);
+
+struct GeneralizedEigenOptions {
+  bool want_vectors = true;
+  // Ridge factors tried in order, scaled by trace(M)/n, before Cholesky is declared failed.
+  double ridge_first = 1e-12;
+  double ridge_retry = 1e-9;
+};
+
+/// A w = lambda M w for Hermitian A and the real symmetric positive definite M (eig.hpp:46-56),
+/// solved on the device (cuSOLVER / cuBLAS; MTNUFFT0): the k_top largest
+/// pairs, values clamped into [0, 1] (SpectralRangeError beyond 1e-6), vectors normalised to
+/// w^* M w = 1 with the canonical phase; ConditioningError when M + ridge is not positive definite.
+EigenPairs generalized_hermitian_eigen(const KernelMatrix& A, const KernelMatrix& M, std::size_t k_top,
+                                       const GeneralizedEigenOptions& opts = {});
+std::vector<double> generalized_hermitian_eigenvalues(const KernelMatrix& A, const KernelMatrix& M,
+                                                      std::size_t k_top,
+                                                      const GeneralizedEigenOptions& opts = {});
 std::vector<double> tridiagonal_eigenvalues(const std::vector<double>& diag,
                                             const std::vector<double>& offdiag);
 

@@ -52,9 +52,15 @@ class MtnufftEstimator {
   SpectrumEstimate estimate(const std::vector<double>& values) const;
   const TaperSet& tapers() const { return tapers_; }
   const NufftPlan& transform_plan() const;
-  EstimatorMethod method() const { return EstimatorMethod::mtnufft; }
+  EstimatorMethod method() const {
+    return opts_.taper_mode == TaperMode::exact_nominal ? EstimatorMethod::mtnufft0 : EstimatorMethod::mtnufft;
+  }
 
  private:
+  struct Built;  // device estimator + its tapers, built together (MTNUFFT0 tapers are O(N^3))
+  static Built build(const SamplingGrid& grid, const SignalBand& signal_band, const BandPlan& plan,
+                     const Options& opts);
+  MtnufftEstimator(const SamplingGrid& grid, const BandPlan& plan, const Options& opts, Built&& built);
   SamplingGrid grid_;
   BandPlan plan_;
   Options opts_;

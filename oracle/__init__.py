@@ -367,6 +367,43 @@ class REF:
         _chk(lib_ref().ref_f_quantile(_d(p), _i64(d1), _i64(d2), ctypes.byref(out)))
         return out.value
 
+    # ---- MTNUFFT0 -------------------------------------------------------
+
+    @staticmethod
+    def generalized_eigen(a, m, k, ridge_first=1e-12, ridge_retry=1e-9, vectors=True):
+        a = np.asarray(a)
+        n = a.shape[0]
+        are = _arr(np.real(a))
+        aim = _arr(np.imag(a)) if np.iscomplexobj(a) else None
+        mm = _arr(m)
+        vals = np.empty(k)
+        vec = np.empty((k, n, 2)) if vectors else None
+        res = np.empty(k)
+        _chk(lib_ref().ref_generalized_eigen(_p(are), _p(aim) if aim is not None else None, _p(mm), _i64(n),
+                                             _i64(k), _d(ridge_first), _d(ridge_retry), _p(vals),
+                                             _p(vec) if vectors else None, _p(res)))
+        return vals, (vec[..., 0] + 1j * vec[..., 1]) if vectors else None, res
+
+    @staticmethod
+    def gpss_exact(t, f_max, f_c, f_w, k):
+        t = _arr(t)
+        w = np.empty((k, t.size, 2))
+        conc = np.empty(k)
+        _chk(lib_ref().ref_gpss_exact(_p(t), _i64(t.size), _d(f_max), _d(f_c), _d(f_w), _i64(k), _p(w),
+                                      _p(conc)))
+        return w[..., 0] + 1j * w[..., 1], conc
+
+    @staticmethod
+    def mtnufft0(t, x, f_max, c, f_w, k, eps, margin=None):
+        t, x, c = _arr(t), _arr(x), _arr(c)
+        p = np.empty(c.size)
+        w = np.empty((k, t.size))
+        method = ctypes.c_int32(-1)
+        _chk(lib_ref().ref_mtnufft0(_p(t), _i64(t.size), _p(x), _d(f_max), _p(c), _i64(c.size), _d(f_w),
+                                    _d(2.0 * f_w if margin is None else margin), _i64(k), _d(eps), _p(p), _p(w),
+                                    ctypes.byref(method)))
+        return p, w, method.value
+
     @staticmethod
     def default_taper_count(tw):
         return int(lib_ref().ref_default_taper_count(tw))

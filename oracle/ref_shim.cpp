@@ -400,6 +400,76 @@ int ref_f_quantile(double p, int64_t d1, int64_t d2, double* out) {
   return guard([&] { *out = f_quantile(p, static_cast<size_t>(d1), static_cast<size_t>(d2)); });
 }
 
+// ---- MTNUFFT0: exact nominal-band GPSS by the dense GEP ----------------
+
+// generalized_hermitian_eigen (eig.cpp:612-659) on dense row-major host matrices
+int ref_generalized_eigen(const double* a_re, const double* a_im /*null: real*/, const double* m, int64_t n,
+                          int64_t k, double ridge_first, double ridge_retry, double* values,
+                          double* vectors /*complex [k][n] or null*/, double* residuals) {
+  return guard([&] {
+    KernelMatrix A(static_cast<size_t>(n), a_im == nullptr, "A");
+    KernelMatrix M(static_cast<size_t>(n), true, "B");
+    std::copy(a_re, a_re + n * n, A.re_data());
+    if (a_im) std::copy(a_im, a_im + n * n, A.im_data());
+    std::copy(m, m + n * n, M.re_data());
+    GeneralizedEigenOptions o;
+    o.ridge_first = ridge_first;
+    o.ridge_retry = ridge_retry;
+    o.want_vectors = vectors != nullptr;
+    const EigenPairs p = generalized_hermitian_eigen(A, M, static_cast<size_t>(k), o);
+    for (size_t j = 0; j < p.count(); ++j) {
+      values[j] = p.values[j];
+      if (vectors) {
+        for (int64_t i = 0; i < n; ++i) {
+          vectors[2 * (j * n + i)] = p.vectors[j][i].real();
+          vectors[2 * (j * n + i) + 1] = p.vectors[j][i].imag();
+        }
+        residuals[j] = p.residuals[j];
+      }
+    }
+  });
+}
+
+// gpss_exact (tapers.cpp:118-144): normalised weights [k][n] complex + concentrations
+int ref_gpss_exact(const double* t, int64_t n, double f_max, double f_c, double f_w, int64_t k, double* w,
+                   double* conc) {
+  return guard([&] {
+    SamplingGrid g(vec(t, n));
+    const TaperSet ts = gpss_exact(g, SignalBand(f_max), AnalysisBand(f_c, f_w), static_cast<size_t>(k));
+    for (size_t j = 0; j < ts.k_tapers(); ++j) {
+      const auto& wj = ts.weights(j);
+      for (int64_t i = 0; i < n; ++i) {
+        w[2 * (j * n + i)] = wj[i].real();
+        w[2 * (j * n + i) + 1] = wj[i].imag();
+      }
+      conc[j] = ts.eigenvalues()[j];
+    }
+  });
+}
+
+// MtnufftEstimator with taper_mode = exact_nominal (estimators.cpp:91-104): MTNUFFT0 P(f)
+int ref_mtnufft0(const double* t, int64_t n, const double* x, double f_max, const double* c, int64_t nc,
+                 double f_w, double margin, int64_t k, double eps, double* power, double* weights /*k x n real*/,
+                 int32_t* method) {
+  return guard([&] {
+    SamplingGrid g(vec(t, n));
+    std::vector<AnalysisBand> bands;
+    for (int64_t i = 0; i < nc; ++i) bands.emplace_back(c[i], f_w);
+    const BandPlan plan(std::move(bands), f_max, margin);
+    MtnufftEstimator::Options o;
+    o.k_tapers = static_cast<size_t>(k);
+    o.epsilon = eps;
+    o.taper_mode = TaperMode::exact_nominal;
+    const MtnufftEstimator est(g, SignalBand(f_max), plan, o);
+    const SpectrumEstimate s = est.estimate(vec(x, n));
+    std::copy(s.power.begin(), s.power.end(), power);
+    if (weights)
+      for (int64_t j = 0; j < k; ++j)
+        for (int64_t i = 0; i < n; ++i) weights[j * n + i] = est.tapers().weights_real(j)[i];
+    *method = static_cast<int32_t>(est.method());
+  });
+}
+
 // ---- reference RNG / grids used by the reference's own tests ---------------
 
 int ref_rng_gauss(uint64_t seed, int64_t count, double* out) {

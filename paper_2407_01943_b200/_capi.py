@@ -48,6 +48,14 @@ class DegenerateTapers(NusError):
     """nuspectral::DegenerateTapers (errors.hpp:36-40)."""
 
 
+class ConditioningError(NumericError):
+    """errors.hpp ConditioningError: metric not positive definite after the ridge retries."""
+
+
+class SpectralRangeError(NumericError):
+    """errors.hpp SpectralRangeError: generalized eigenvalue outside [0, 1] beyond 1e-6."""
+
+
 class CudaError(NusError):
     pass
 
@@ -61,7 +69,7 @@ class NoDeviceError(CudaError):
 
 
 _ERRORS = {1: InvalidArgument, 2: PlanMismatch, 3: BandRangeError, 4: ExtrapolationError,
-           5: NumericError, 6: CudaError, 7: OutOfMemory, 8: NoDeviceError, 9: DegenerateTapers}
+           5: NumericError, 6: CudaError, 7: OutOfMemory, 8: NoDeviceError, 9: DegenerateTapers, 10: ConditioningError, 11: SpectralRangeError}
 
 _i64 = ctypes.c_int64
 _i32 = ctypes.c_int32
@@ -114,6 +122,9 @@ _SIGS = {
     "nus_mtnufft_estimate_device": [_vp, _vp, _i32, _vp, _vp, _vp],
     "nus_mtnufft_spread_device": [_vp, _vp, _i32, _i64, _i64, _vp, _i64, _vp],
     "nus_mtnufft_stage_kernels": [_vp, ctypes.c_char_p, _i64],
+    "nus_generalized_eigen": [_dp, _dp, _dp, _i64, _i64, _d, _d, _i32, _i32, _dp, _dp, _dp],
+    "nus_gpss_exact": [_dp, _i64, _d, _d, _d, _i64, _d, _d, _i32, _dp, _dp],
+    "nus_band_matrix": [_dp, _i64, _d, _d, _i32, _dp, _dp],
     "nus_mtnufft_transform_device": [_vp, _vp, _i64, _i64, _d, _i32, _vp, _vp],
     "nus_mtnufft_bytes_model": [_vp, _i32, _dp, _dp, _dp, _dp],
     "nus_f_test": [_dp, _i64, _i64, _dp, _i64, _dp, _d, _d, _i32, _dp, _dp, ctypes.POINTER(ctypes.c_uint8)],

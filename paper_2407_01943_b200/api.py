@@ -18,8 +18,8 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 from . import _capi as C
-from ._capi import (BandRangeError, DegenerateTapers, ExtrapolationError, InvalidArgument,
-                    NoDeviceError, NusError, NumericError, PlanMismatch)
+from ._capi import (BandRangeError, ConditioningError, DegenerateTapers, ExtrapolationError, InvalidArgument,
+                    NoDeviceError, NusError, NumericError, PlanMismatch, SpectralRangeError)
 
 __all__ = [
     "SamplingGrid", "SignalSeries", "SignalBand", "AnalysisBand", "BandPlan", "make_band_plan",
@@ -30,6 +30,8 @@ __all__ = [
     "NusError", "InvalidArgument", "PlanMismatch", "BandRangeError", "ExtrapolationError",
     "NumericError", "NoDeviceError", "Precision", "DegenerateTapers", "FTestResult", "FTestOptions",
     "f_test", "f_quantile", "kFtestConditionViolated", "kFtestSaturated",
+    "GeneralizedEigenOptions", "generalized_hermitian_eigen", "gpss_exact", "EigenPairs",
+    "ConditioningError", "SpectralRangeError",
 ]
 
 kBandBoundary = 1  # grid.hpp:10
@@ -354,9 +356,8 @@ class TaperSet:
             raise InvalidArgument("TaperSet: taper length mismatch")
         if eigenvalues is not None and len(eigenvalues) and len(eigenvalues) != w.shape[0]:
             raise InvalidArgument("TaperSet: eigenvalue count mismatch")
-        if not is_real:
-            raise InvalidArgument("TaperSet: complex tapers are outside the MTNUFFT path")
         self._grid, self._band, self._f_max = grid, band, float(f_max)
+        self._real = bool(is_real)
         self._w = w
         self._ev = np.array(eigenvalues if eigenvalues is not None else [], dtype=np.float64)
 
@@ -376,7 +377,7 @@ class TaperSet:
         return self._f_max
 
     def is_real(self):
-        return True
+        return self._real
 
     def has_eigenvalues(self):
         return self._ev.size > 0
@@ -388,6 +389,8 @@ class TaperSet:
         return self._w[k].astype(np.complex128)
 
     def weights_real(self, k):
+        if not self._real:
+            raise InvalidArgument("TaperSet: weights_real on complex tapers")
         return self._w[k]
 
     def weights_matrix(self):
@@ -425,6 +428,58 @@ def gpss_interpolated(grid: SamplingGrid, signal_band: SignalBand, f_w: float, k
     C.check(C.lib().nus_gpss_interpolated(C.dptr(t), t.size, signal_band.f_max, float(f_w), k_tapers,
                                           device, C.dptr(w)))
     return TaperSet(grid, AnalysisBand(0.0, f_w), signal_band.f_max, w, None, True)
+
+
+@dataclass
+class GeneralizedEigenOptions:
+    """eig.hpp:38-44."""
+    want_vectors: bool = True
+    ridge_first: float = 1e-12
+    ridge_retry: float = 1e-9
+
+
+def generalized_hermitian_eigen(a, m, k_top: int, opts: Optional[GeneralizedEigenOptions] = None,
+                                device: int = 0) -> EigenPairs:
+    """A w = lambda M w on the device (eig.cpp:612-659): Cholesky with ridge, dense Hermitian
+    eigensolve (cuSOLVER), the k largest pairs with values clamped into [0, 1], M-normalised
+    vectors with the canonical phase, residuals ||A w - lambda M w|| / (||A||_F ||w||)."""
+    opts = opts or GeneralizedEigenOptions()
+    a = np.asarray(a)
+    m = C.f64(m)
+    if a.ndim != 2 or a.shape[0] != a.shape[1] or m.shape != a.shape:
+        raise InvalidArgument("generalized_hermitian_eigen: size mismatch")
+    if np.iscomplexobj(m) or np.iscomplexobj(np.asarray(m)):
+        raise InvalidArgument("generalized_hermitian_eigen: metric must be the real signal-band kernel")
+    if k_top < 1:
+        raise InvalidArgument("generalized_hermitian_eigen: k_top must be >= 1")
+    n = a.shape[0]
+    k = min(int(k_top), n)
+    are = C.f64(np.real(a))
+    aim = C.f64(np.imag(a)) if np.iscomplexobj(a) else None
+    vals, res = np.empty(k), np.empty(k)
+    vecs = np.empty((k, n, 2))
+    C.check(C.lib().nus_generalized_eigen(C.dptr(are), C.dptr(aim) if aim is not None else None, C.dptr(m), n, k,
+                                          opts.ridge_first, opts.ridge_retry, 1 if opts.want_vectors else 0, device,
+                                          C.dptr(vals), C.dptr(vecs), C.dptr(res)))
+    if not opts.want_vectors:
+        return EigenPairs(vals, np.empty((0, n), np.complex128), np.empty(0))
+    return EigenPairs(vals, vecs[..., 0] + 1j * vecs[..., 1], res)
+
+
+def gpss_exact(grid: SamplingGrid, signal_band: SignalBand, band: AnalysisBand, k_tapers: int,
+               opts: Optional[GeneralizedEigenOptions] = None, device: int = 0) -> TaperSet:
+    """Exact nominal-band GPSS tapers (tapers.cpp:118-144): R(A) w = lambda R(B) w on the device,
+    each taper scaled to w^H R(B) w = 2 f_w.  Real for a band centred at 0."""
+    opts = opts or GeneralizedEigenOptions()
+    t = C.f64(grid.times())
+    k = int(k_tapers)
+    w = np.empty((max(k, 1), t.size, 2))
+    conc = np.empty(max(k, 1))
+    C.check(C.lib().nus_gpss_exact(C.dptr(t), t.size, signal_band.f_max, band.f_center, band.half_width, k,
+                                   opts.ridge_first, opts.ridge_retry, device, C.dptr(w), C.dptr(conc)))
+    real_band = band.f_center == 0.0
+    wc = w[..., 0] + 1j * w[..., 1]
+    return TaperSet(grid, band, signal_band.f_max, wc.real.copy() if real_band else wc, conc, real_band)
 
 
 def default_taper_count(time_half_bandwidth: float) -> int:  # tapers.cpp:219-222
@@ -556,10 +611,17 @@ class MtnufftEstimator:
     def __init__(self, grid: SamplingGrid, signal_band: SignalBand, plan: BandPlan,
                  opts: Optional["MtnufftEstimator.Options"] = None, tapers=None):
         opts = opts or MtnufftEstimator.Options()
-        if opts.taper_mode != "interpolated":
-            raise InvalidArgument("MtnufftEstimator: only the interpolated taper mode is on the "
-                                  "B200 path (mtnufft0 is out of scope)")
+        if opts.taper_mode not in ("interpolated", "exact_nominal"):
+            raise InvalidArgument(f"MtnufftEstimator: unknown taper mode {opts.taper_mode!r}")
         self._grid, self._plan, self._opts = grid, plan, opts
+        self._method = "mtnufft"
+        self._conc = None
+        if opts.taper_mode == "exact_nominal" and tapers is None:
+            # MTNUFFT0 (estimators.cpp:91-104): exact nominal-band tapers from the dense GEP
+            ts = gpss_exact(grid, signal_band, AnalysisBand(0.0, plan.half_width()), opts.k_tapers,
+                            device=opts.device)
+            tapers, self._conc = ts.weights_matrix(), ts.eigenvalues()
+            self._method = "mtnufft0"
         self._est = _Estimator(grid.times(), plan.centers(), signal_band.f_max, plan.half_width(),
                                opts.k_tapers, opts.epsilon, int(opts.path_policy), opts.precision,
                                opts.device, tapers=tapers)
@@ -572,7 +634,7 @@ class MtnufftEstimator:
         bands = self._plan.size()
         if np.any(~(p >= 0.0)):
             raise InvalidArgument("SpectrumEstimate: negative power")
-        return SpectrumEstimate(self._plan, p, "mtnufft", np.full(bands, self._opts.k_tapers),
+        return SpectrumEstimate(self._plan, p, self._method, np.full(bands, self._opts.k_tapers),
                                 np.full(bands, self._plan.half_width()), self._plan.flags())
 
     def eigencoefficients(self, values) -> EigenCoefficients:
@@ -593,13 +655,13 @@ class MtnufftEstimator:
 
     def tapers(self) -> TaperSet:
         w = self._est.tapers()[0]
-        return TaperSet(self._grid, AnalysisBand(0.0, self._plan.half_width()), self._plan.f_max, w)
+        return TaperSet(self._grid, AnalysisBand(0.0, self._plan.half_width()), self._plan.f_max, w, self._conc)
 
     def transform_info(self):
         return self._est.info
 
     def method(self) -> str:
-        return "mtnufft"
+        return self._method
 
     def setup_ms(self):
         return self._est.setup_ms()

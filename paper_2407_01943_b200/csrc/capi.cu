@@ -267,6 +267,57 @@ int nus_signal_band_matrix(const double* times, int64_t n, double f_max, int32_t
   });
 }
 
+// ---- MTNUFFT0: exact nominal-band GPSS (gep.cu) -------------------------
+
+int nus_generalized_eigen(const double* a_re, const double* a_im, const double* m, int64_t n, int64_t k,
+                          double ridge_first, double ridge_retry, int32_t want_vectors, int32_t device,
+                          double* values, double* vectors, double* residuals) {
+  return guarded([&] {
+    nus::require(a_re && m && values, "generalized_hermitian_eigen: null argument");
+    nus::require(!want_vectors || (vectors && residuals), "generalized_hermitian_eigen: null vector output");
+    nus::require(n >= 1 && k >= 1, "generalized_hermitian_eigen: k_top must be >= 1");
+    nus::use_device(device);
+    const size_t nn = static_cast<size_t>(n) * n;
+    nus::DeviceBuffer dre(nn * sizeof(double)), dm(nn * sizeof(double)), dim(a_im ? nn * sizeof(double) : 0);
+    NUS_CUDA(cudaMemcpy(dre.ptr, a_re, dre.bytes, cudaMemcpyHostToDevice));
+    NUS_CUDA(cudaMemcpy(dm.ptr, m, dm.bytes, cudaMemcpyHostToDevice));
+    if (a_im) {  // row-major Hermitian read column-major is conj(A): flip the imaginary part
+      std::vector<double> neg(a_im, a_im + nn);
+      for (double& v : neg) v = -v;
+      NUS_CUDA(cudaMemcpy(dim.ptr, neg.data(), dim.bytes, cudaMemcpyHostToDevice));
+    }
+    nus::generalized_eigen_device(dre.as<double>(), a_im ? dim.as<double>() : nullptr, dm.as<double>(), n, k,
+                                  ridge_first, ridge_retry, want_vectors != 0, values, vectors, residuals);
+  });
+}
+
+int nus_band_matrix(const double* times, int64_t n, double f_w, double f_center, int32_t device, double* re_out,
+                    double* im_out) {
+  return guarded([&] {
+    nus::require(times && re_out, "analysis_band_kernel: null argument");
+    nus::require(n >= 1, "analysis_band_kernel: empty grid");
+    nus::use_device(device);
+    const size_t nn = static_cast<size_t>(n) * n;
+    nus::DeviceBuffer t(n * sizeof(double)), re(nn * sizeof(double)), im(im_out ? nn * sizeof(double) : 0);
+    NUS_CUDA(cudaMemcpy(t.ptr, times, t.bytes, cudaMemcpyHostToDevice));
+    const double mean_dt = (times[n - 1] - times[0]) / static_cast<double>(n);
+    nus::band_matrix_rowmajor(t.as<double>(), n, f_w, f_center, 1e-12 * mean_dt, re.as<double>(),
+                              im_out ? im.as<double>() : nullptr);
+    NUS_CUDA(cudaMemcpy(re_out, re.ptr, re.bytes, cudaMemcpyDeviceToHost));
+    if (im_out) NUS_CUDA(cudaMemcpy(im_out, im.ptr, im.bytes, cudaMemcpyDeviceToHost));
+  });
+}
+
+int nus_gpss_exact(const double* times, int64_t n, double f_max, double f_center, double f_w, int64_t k,
+                   double ridge_first, double ridge_retry, int32_t device, double* w_out, double* concentrations) {
+  return guarded([&] {
+    nus::require(times && w_out && concentrations, "gpss_exact: null argument");
+    nus::require(n >= 2, "gpss_exact: need at least 2 samples");
+    nus::use_device(device);
+    nus::gpss_exact_device(times, n, f_max, f_center, f_w, k, ridge_first, ridge_retry, w_out, concentrations);
+  });
+}
+
 // ---- tapers -----------------------------------------------------------------------
 
 int nus_dpss(int64_t n, double tw, int64_t k, int32_t device, double* tapers_host,

@@ -1,6 +1,7 @@
 // MtnufftEstimator of the drop-in (reference behaviour: src/estimators.cpp:66-122,261-270).
 #include "nuspectral/estimators.hpp"
 
+#include <algorithm>
 #include <stdexcept>
 #include <utility>
 
@@ -39,17 +40,19 @@ SpectrumEstimate::SpectrumEstimate(BandPlan p, std::vector<double> pw, Estimator
       throw std::invalid_argument("SpectrumEstimate: negative power");
 }
 
+struct MtnufftEstimator::Built {
+  std::shared_ptr<nus_mtnufft_s> handle;
+  TaperSet tapers;
+};
+
 namespace {
 
-std::shared_ptr<nus_mtnufft_s> make_estimator(const SamplingGrid& grid, const SignalBand& band,
-                                              const BandPlan& plan, const MtnufftEstimator::Options& o) {
-  if (o.taper_mode != TaperMode::interpolated)
-    throw std::invalid_argument("MtnufftEstimator: exact_nominal (MTNUFFT0) tapers are outside the B200 path");
-  const std::vector<double> centers = plan.centers();
+nus_mtnufft_config_t make_config(const SamplingGrid& grid, const SignalBand& band, const BandPlan& plan,
+                                 const MtnufftEstimator::Options& o, std::size_t n_centers) {
   nus_mtnufft_config_t cfg{};
   cfg.channels = 1;
   cfg.n = static_cast<int64_t>(grid.n_samples());
-  cfg.n_centers = static_cast<int64_t>(centers.size());
+  cfg.n_centers = static_cast<int64_t>(n_centers);
   cfg.k_tapers = static_cast<int64_t>(o.k_tapers);
   cfg.f_max = band.f_max;
   cfg.f_w = plan.half_width();
@@ -59,30 +62,50 @@ std::shared_ptr<nus_mtnufft_s> make_estimator(const SamplingGrid& grid, const Si
                                                                 : NUS_AUTO_SELECT;
   cfg.precision = NUS_F64;
   cfg.device = host::device();
-  if (o.k_tapers < 1 || o.k_tapers > grid.n_samples())
-    throw std::invalid_argument("dpss_uniform: k_tapers out of range");
-  nus_mtnufft_t h = nullptr;
-  host::check(nus_mtnufft_create(&cfg, grid.times().data(), centers.data(), nullptr, &h));
-  return std::shared_ptr<nus_mtnufft_s>(h, [](nus_mtnufft_s* p) { nus_mtnufft_destroy(p); });
+  return cfg;
 }
 
-TaperSet fetch_tapers(const std::shared_ptr<nus_mtnufft_s>& h, const SamplingGrid& grid, const SignalBand& band,
-                      const BandPlan& plan, std::size_t k) {
-  const std::size_t n = grid.n_samples();
-  std::vector<double> w(k * n);
-  host::check(nus_mtnufft_tapers(h.get(), w.data()));
-  std::vector<std::vector<std::complex<double>>> weights(k, std::vector<std::complex<double>>(n));
-  for (std::size_t j = 0; j < k; ++j)
-    for (std::size_t i = 0; i < n; ++i) weights[j][i] = {w[j * n + i], 0.0};
-  return TaperSet(grid, AnalysisBand(0.0, plan.half_width()), band.f_max, std::move(weights), {}, true);
+std::shared_ptr<nus_mtnufft_s> wrap(nus_mtnufft_t h) {
+  return std::shared_ptr<nus_mtnufft_s>(h, [](nus_mtnufft_s* p) { nus_mtnufft_destroy(p); });
 }
 
 }  // namespace
 
+// Tapers first, then the transform plan (estimators.cpp:91-104): interpolated prolates
+// (MTNUFFT) are built inside the device estimator; the exact nominal-band tapers (MTNUFFT0)
+// come from gpss_exact on the dense pencil and are handed to the estimator.
+MtnufftEstimator::Built MtnufftEstimator::build(const SamplingGrid& grid, const SignalBand& band,
+                                                const BandPlan& plan, const Options& o) {
+  const std::vector<double> centers = plan.centers();
+  const nus_mtnufft_config_t cfg = make_config(grid, band, plan, o, centers.size());
+  const std::size_t n = grid.n_samples(), k = o.k_tapers;
+  nus_mtnufft_t h = nullptr;
+  if (o.taper_mode == TaperMode::exact_nominal) {
+    TaperSet ts = gpss_exact(grid, band, AnalysisBand(0.0, plan.half_width()), k);
+    std::vector<double> w(k * n);
+    for (std::size_t j = 0; j < k; ++j) std::copy(ts.weights_real(j).begin(), ts.weights_real(j).end(), w.begin() + j * n);
+    host::check(nus_mtnufft_create(&cfg, grid.times().data(), centers.data(), w.data(), &h));
+    return {wrap(h), std::move(ts)};
+  }
+  if (k < 1 || k > n) throw std::invalid_argument("dpss_uniform: k_tapers out of range");
+  host::check(nus_mtnufft_create(&cfg, grid.times().data(), centers.data(), nullptr, &h));
+  auto handle = wrap(h);
+  std::vector<double> w(k * n);
+  host::check(nus_mtnufft_tapers(handle.get(), w.data()));
+  std::vector<std::vector<std::complex<double>>> weights(k, std::vector<std::complex<double>>(n));
+  for (std::size_t j = 0; j < k; ++j)
+    for (std::size_t i = 0; i < n; ++i) weights[j][i] = {w[j * n + i], 0.0};
+  return {std::move(handle),
+          TaperSet(grid, AnalysisBand(0.0, plan.half_width()), band.f_max, std::move(weights), {}, true)};
+}
+
 MtnufftEstimator::MtnufftEstimator(const SamplingGrid& grid, const SignalBand& signal_band, const BandPlan& plan,
                                    const Options& opts)
-    : grid_(grid), plan_(plan), opts_(opts), handle_(make_estimator(grid, signal_band, plan, opts)),
-      tapers_(fetch_tapers(handle_, grid, signal_band, plan, opts.k_tapers)) {}
+    : MtnufftEstimator(grid, plan, opts, build(grid, signal_band, plan, opts)) {}
+
+MtnufftEstimator::MtnufftEstimator(const SamplingGrid& grid, const BandPlan& plan, const Options& opts,
+                                   Built&& built)
+    : grid_(grid), plan_(plan), opts_(opts), handle_(std::move(built.handle)), tapers_(std::move(built.tapers)) {}
 
 SpectrumEstimate MtnufftEstimator::estimate(const std::vector<double>& values) const {
   if (values.size() != grid_.n_samples())
@@ -90,7 +113,7 @@ SpectrumEstimate MtnufftEstimator::estimate(const std::vector<double>& values) c
   std::vector<double> power(plan_.size());
   host::check(nus_mtnufft_estimate(handle_.get(), values.data(), power.data()));
   const std::size_t bands = plan_.size();
-  return SpectrumEstimate(plan_, std::move(power), EstimatorMethod::mtnufft,
+  return SpectrumEstimate(plan_, std::move(power), method(),
                           std::vector<std::size_t>(bands, opts_.k_tapers),
                           std::vector<double>(bands, plan_.half_width()), plan_.flags());
 }

@@ -200,4 +200,52 @@ KernelMatrix signal_band_kernel(const SamplingGrid& grid, const SignalBand& band
   return m;
 }
 
+KernelMatrix analysis_band_kernel(const SamplingGrid& grid, const AnalysisBand& band) {
+  const std::size_t n = grid.n_samples();
+  const bool real = band.f_center == 0.0;
+  KernelMatrix m(n, real, real ? "A0" : "A");
+  host::check(nus_band_matrix(grid.times().data(), static_cast<int64_t>(n), band.half_width, band.f_center,
+                              host::device(), m.re_data(), real ? nullptr : m.im_data()));
+  return m;
+}
+
+namespace {
+EigenPairs generalized(const KernelMatrix& A, const KernelMatrix& M, std::size_t k_top,
+                       const GeneralizedEigenOptions& opts) {
+  if (A.n() != M.n()) throw std::invalid_argument("generalized_hermitian_eigen: size mismatch");
+  if (!M.is_real())
+    throw std::invalid_argument("generalized_hermitian_eigen: metric must be the real signal-band kernel");
+  if (k_top == 0) throw std::invalid_argument("generalized_hermitian_eigen: k_top must be >= 1");
+  const std::size_t n = A.n(), k = std::min(k_top, n);
+  std::vector<double> vals(k), vecs(opts.want_vectors ? 2 * k * n : 0), res(opts.want_vectors ? k : 0);
+  host::check(nus_generalized_eigen(A.re_data(), A.is_real() ? nullptr : A.im_data(), M.re_data(),
+                                    static_cast<int64_t>(n), static_cast<int64_t>(k), opts.ridge_first,
+                                    opts.ridge_retry, opts.want_vectors ? 1 : 0, host::device(), vals.data(),
+                                    opts.want_vectors ? vecs.data() : nullptr,
+                                    opts.want_vectors ? res.data() : nullptr));
+  EigenPairs out;
+  out.metric = EigenMetric::rb_metric;
+  out.values = std::move(vals);
+  if (opts.want_vectors) {
+    out.vectors.assign(k, std::vector<std::complex<double>>(n));
+    for (std::size_t j = 0; j < k; ++j)
+      for (std::size_t i = 0; i < n; ++i) out.vectors[j][i] = {vecs[2 * (j * n + i)], vecs[2 * (j * n + i) + 1]};
+    out.residuals = std::move(res);
+  }
+  return out;
+}
+}  // namespace
+
+EigenPairs generalized_hermitian_eigen(const KernelMatrix& A, const KernelMatrix& M, std::size_t k_top,
+                                       const GeneralizedEigenOptions& opts) {
+  return generalized(A, M, k_top, opts);
+}
+
+std::vector<double> generalized_hermitian_eigenvalues(const KernelMatrix& A, const KernelMatrix& M,
+                                                      std::size_t k_top, const GeneralizedEigenOptions& opts) {
+  GeneralizedEigenOptions o = opts;
+  o.want_vectors = false;
+  return generalized(A, M, k_top, o).values;
+}
+
 }  // namespace nuspectral

@@ -20,6 +20,8 @@ inline void check(int rc) {
     case NUS_ERR_EXTRAPOLATION: throw ExtrapolationError(msg);
     case NUS_ERR_NUMERIC: throw Error(msg);
     case NUS_ERR_DEGENERATE_TAPERS: throw DegenerateTapers(msg);
+    case NUS_ERR_CONDITIONING: throw ConditioningError(msg);
+    case NUS_ERR_SPECTRAL_RANGE: throw SpectralRangeError(msg);
     case NUS_ERR_OUT_OF_MEMORY: throw DeviceError("out of device memory: " + msg);
     default: throw DeviceError(msg);
   }

@@ -63,6 +63,21 @@ TaperSet gpss_interpolated(const SamplingGrid& grid, const SignalBand& signal_ba
   return TaperSet(grid, AnalysisBand(0.0, f_w), signal_band.f_max, std::move(weights), {}, true);
 }
 
+TaperSet gpss_exact(const SamplingGrid& grid, const SignalBand& signal_band, const AnalysisBand& band,
+                    std::size_t k_tapers, const GeneralizedEigenOptions& opts) {
+  const std::size_t n = grid.n_samples();
+  const std::size_t k = std::max<std::size_t>(k_tapers, 1);
+  std::vector<double> w(2 * k * n), conc(k);
+  host::check(nus_gpss_exact(grid.times().data(), static_cast<int64_t>(n), signal_band.f_max, band.f_center,
+                             band.half_width, static_cast<int64_t>(k_tapers), opts.ridge_first, opts.ridge_retry,
+                             host::device(), w.data(), conc.data()));
+  std::vector<std::vector<std::complex<double>>> weights(k_tapers, std::vector<std::complex<double>>(n));
+  for (std::size_t j = 0; j < k_tapers; ++j)
+    for (std::size_t i = 0; i < n; ++i) weights[j][i] = {w[2 * (j * n + i)], w[2 * (j * n + i) + 1]};
+  conc.resize(k_tapers);
+  return TaperSet(grid, band, signal_band.f_max, std::move(weights), std::move(conc), band.f_center == 0.0);
+}
+
 std::size_t default_taper_count(double time_half_bandwidth) {
   const long k = std::lround(2.0 * time_half_bandwidth) - 1;
   return static_cast<std::size_t>(std::max(k, 1L));

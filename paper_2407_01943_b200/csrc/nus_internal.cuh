@@ -170,6 +170,14 @@ void run_crop(Plan& plan, void* grid, int64_t k, int64_t kpad, void* j_out, void
 
 // Fused two-pass FFT + crop/power (fft.cu); supported for 32 <= Mr <= 2^24.
 bool fused_fft_supported(const PlanParams& p);
+// MTNUFFT0 (gep.cu)
+void generalized_eigen_device(const double* d_are, const double* d_aim, const double* d_m, int64_t n, int64_t k,
+                              double ridge_first, double ridge_retry, bool want_vectors, double* values,
+                              double* vectors, double* residuals);
+void band_matrix_rowmajor(const double* d_t, int64_t n, double f, double fc, double tol, double* d_re,
+                          double* d_im);
+void gpss_exact_device(const double* h_t, int64_t n, double f_max, double f_c, double f_w, int64_t k,
+                       double ridge_first, double ridge_retry, double* w_out, double* conc);
 const char* spread_kernel_name();
 void fft_stage_names(const Plan& plan, const char** pass_a, const char** pass_b);
 void fused_fft_prepare(Plan& plan);

@@ -559,6 +559,119 @@ double host_ms_since(std::chrono::steady_clock::time_point t0) {
 
 // ---------------------------------------------------------------- tridiagonal top-K
 
+// Eigenvectors of (near-)degenerate eigenvalues (|lambda_p - lambda_j| <= 1e-13 ||T||), following the
+// reference's inverse iteration (eig.cpp:217-279) so that degenerate spectra give the same
+// basis: start at the unused coordinate whose diagonal is nearest lambda (chosen on the host,
+// in order over all k vectors), shift lambda + ||T|| eps 10 (rank + 1), up to 6 iterations
+// of (partially pivoted solve, normalise, re-orthogonalise against the earlier cluster
+// members, normalise), stop at residual <= 1e-11 ||T||.  One block per cluster (members in
+// index order); thread 0 runs the sequential solve, the block the reductions.  fp64.
+namespace {
+constexpr int kClusterThreads = 256;
+
+__device__ double block_sum(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int w = 0; w < kClusterThreads / 32; ++w) t += red[w];
+  return t;
+}
+
+__global__ void cluster_inverse_iteration_kernel(const double* __restrict__ d, const double* __restrict__ e,
+                                                 int64_t n, const int32_t* __restrict__ offs,
+                                                 const int32_t* __restrict__ members,
+                                                 const int32_t* __restrict__ starts, const double* __restrict__ lam,
+                                                 const double* __restrict__ lam_solve, double anorm, double pivmin,
+                                                 double* __restrict__ vec, double* __restrict__ scratch) {
+  __shared__ double red[kClusterThreads / 32];
+  const int c = blockIdx.x;
+  const int m0 = offs[c], m1 = offs[c + 1];
+  double* u0 = scratch + static_cast<int64_t>(c) * 3 * n;
+  double* u1 = u0 + n;
+  double* u2 = u1 + n;
+  const double cluster_tol = anorm * 1e-8, accept = anorm * 1e-11;
+  for (int q = m0; q < m1; ++q) {
+    const int j = members[q];
+    double* x = vec + static_cast<int64_t>(j) * n;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) x[i] = i == starts[q] ? 1.0 : 0.0;
+    __syncthreads();
+    for (int it = 0; it < 6; ++it) {
+      if (threadIdx.x == 0) {  // solve_shifted_tridiag (eig.cpp:119-168)
+        const double ls = lam_solve[q];
+        if (n == 1) {
+          double p = d[0] - ls;
+          if (fabs(p) < pivmin) p = copysign(pivmin, p == 0.0 ? 1.0 : p);
+          x[0] /= p;
+        } else {
+          double c0 = d[0] - ls, c1 = e[0], c2 = 0.0;
+          for (int64_t i = 0; i + 1 < n; ++i) {
+            const double sub = e[i], dd = d[i + 1] - ls, sup = (i + 2 < n) ? e[i + 1] : 0.0;
+            if (fabs(sub) > fabs(c0)) {
+              u0[i] = sub;
+              u1[i] = dd;
+              u2[i] = sup;
+              const double mm = c0 / sub;
+              const double t = x[i];
+              x[i] = x[i + 1];
+              x[i + 1] = t - mm * x[i];
+              c0 = c1 - mm * dd;
+              c1 = c2 - mm * sup;
+              c2 = 0.0;
+            } else {
+              if (fabs(c0) < pivmin) c0 = copysign(pivmin, c0 == 0.0 ? 1.0 : c0);
+              u0[i] = c0;
+              u1[i] = c1;
+              u2[i] = c2;
+              const double mm = sub / c0;
+              x[i + 1] -= mm * x[i];
+              c0 = dd - mm * c1;
+              c1 = sup - mm * c2;
+              c2 = 0.0;
+            }
+          }
+          if (fabs(c0) < pivmin) c0 = copysign(pivmin, c0 == 0.0 ? 1.0 : c0);
+          u0[n - 1] = c0;
+          x[n - 1] /= u0[n - 1];
+          x[n - 2] = (x[n - 2] - u1[n - 2] * x[n - 1]) / u0[n - 2];
+          for (int64_t i = n - 2; i-- > 0;) x[i] = (x[i] - u1[i] * x[i + 1] - u2[i] * x[i + 2]) / u0[i];
+        }
+      }
+      __syncthreads();
+      for (int pass = 0; pass < 2; ++pass) {  // normalise, re-orthogonalise, normalise
+        double s2 = 0.0;
+        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s2 += x[i] * x[i];
+        const double nrm = sqrt(block_sum(s2, red));
+        if (nrm > 0.0)
+          for (int64_t i = threadIdx.x; i < n; i += blockDim.x) x[i] /= nrm;
+        __syncthreads();
+        if (pass == 1) break;
+        for (int p = m0; p < q; ++p) {
+          if (fabs(lam[p] - lam[q]) > cluster_tol) continue;
+          const double* xp = vec + static_cast<int64_t>(members[p]) * n;
+          double dot = 0.0;
+          for (int64_t i = threadIdx.x; i < n; i += blockDim.x) dot += x[i] * xp[i];
+          const double proj = block_sum(dot, red);
+          for (int64_t i = threadIdx.x; i < n; i += blockDim.x) x[i] -= proj * xp[i];
+          __syncthreads();
+        }
+      }
+      double r2 = 0.0;  // tridiag_residual
+      for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        double t = (d[i] - lam[q]) * x[i];
+        if (i > 0) t += e[i - 1] * x[i - 1];
+        if (i + 1 < n) t += e[i] * x[i + 1];
+        r2 += t * t;
+      }
+      const double resid = sqrt(block_sum(r2, red));
+      if (resid <= accept) break;
+    }
+    __syncthreads();
+  }
+}
+}  // namespace
+
 DpssResult tridiag_top_device(const double* d_diag, const double* d_off, int64_t n, int64_t k,
                               double* d_vec, cudaStream_t s) {
   require(k >= 1 && k <= n, "tridiagonal_eigen: k_top out of range");
@@ -626,8 +739,21 @@ DpssResult tridiag_top_device(const double* d_diag, const double* d_off, int64_t
   DpssResult res;
   res.values.resize(k);
   std::vector<double> sig_hi(k), sig_lo(k);
+  // a diagonal entry split off by negligible off-diagonals (the QL deflation rule,
+  // |e_i| <= eps (|d_i| + |d_i+1|)) is an exact eigenvalue: return it exactly, as the reference
+  std::vector<double> isolated;
+  for (int64_t i = 0; i < n; ++i) {
+    const bool lo_split = i == 0 || std::fabs(he[i - 1]) <= DBL_EPSILON * (std::fabs(hd[i - 1]) + std::fabs(hd[i]));
+    const bool hi_split = i + 1 >= n || std::fabs(he[i]) <= DBL_EPSILON * (std::fabs(hd[i]) + std::fabs(hd[i + 1]));
+    if (lo_split && hi_split) isolated.push_back(hd[i]);
+  }
   for (int64_t j = 0; j < k; ++j) {
-    const double mid = 0.5 * (lo[j] + hi[j]);
+    double mid = 0.5 * (lo[j] + hi[j]);
+    for (const double v : isolated)
+      if (v >= lo[j] - target && v <= hi[j] + target) {
+        mid = v;
+        break;
+      }
     res.values[j] = mid;
     sig_hi[j] = mid;
     sig_lo[j] = 0.0;
@@ -645,6 +771,73 @@ DpssResult tridiag_top_device(const double* d_diag, const double* d_off, int64_t
   dd_finalize_kernel<<<blocks_for(n * k, 256), 256, 0, s>>>(xs.as<dd>(), d_norm.as<double>(), n,
                                                             static_cast<int>(k), d_vec);
   note_launch();
+  {
+    // (near-)degenerate eigenvalues, which no inverse iteration separates: the reference's
+    // start-vector / re-orthogonalisation rule.  Pairs the double-double iteration resolves
+    // (DPSS gaps are ~1e-8 ||T|| at N = 2^16) keep the fast path: their eigenvectors are unique.
+    const double cluster_tol = anorm * 1e-13;
+    std::vector<int32_t> offs{0}, members, starts;
+    std::vector<double> lam, lam_solve;
+    std::vector<char> used(n, 0);
+    std::vector<int64_t> best(k);
+    for (int64_t j = 0; j < k; ++j) {  // nearest unused diagonal, in order (eig.cpp:234-245)
+      int64_t b = n;
+      double gap = 0.0;
+      for (int64_t i = 0; i < n; ++i) {
+        if (used[i]) continue;
+        const double g = std::fabs(hd[i] - res.values[j]);
+        if (b == n || g < gap) {
+          b = i;
+          gap = g;
+        }
+      }
+      if (b == n) b = j % n;
+      used[b] = 1;
+      best[j] = b;
+    }
+    std::vector<char> done(k, 0);
+    for (int64_t j = 0; j < k; ++j) {
+      if (done[j]) continue;
+      // connected component of the "within cluster_tol" relation starting at j
+      std::vector<int64_t> comp{j};
+      done[j] = 1;
+      for (size_t a = 0; a < comp.size(); ++a)
+        for (int64_t p = 0; p < k; ++p)
+          if (!done[p] && std::fabs(res.values[p] - res.values[comp[a]]) <= cluster_tol) {
+            done[p] = 1;
+            comp.push_back(p);
+          }
+      if (comp.size() < 2) continue;
+      std::sort(comp.begin(), comp.end());
+      for (const int64_t q : comp) {
+        int64_t rank = 0;
+        for (int64_t p = 0; p < q; ++p)
+          if (std::fabs(res.values[p] - res.values[q]) <= cluster_tol) ++rank;
+        members.push_back(static_cast<int32_t>(q));
+        starts.push_back(static_cast<int32_t>(best[q]));
+        lam.push_back(res.values[q]);
+        lam_solve.push_back(res.values[q] + anorm * DBL_EPSILON * 10.0 * static_cast<double>(rank + 1));
+      }
+      offs.push_back(static_cast<int32_t>(members.size()));
+    }
+    const int ncl = static_cast<int>(offs.size()) - 1;
+    if (ncl > 0) {
+      DeviceBuffer d_offs(offs.size() * sizeof(int32_t)), d_mem(members.size() * sizeof(int32_t)),
+          d_st(starts.size() * sizeof(int32_t)), d_lam(lam.size() * sizeof(double)),
+          d_ls(lam_solve.size() * sizeof(double)), scr(static_cast<size_t>(ncl) * 3 * n * sizeof(double));
+      NUS_CUDA(cudaMemcpyAsync(d_offs.ptr, offs.data(), d_offs.bytes, cudaMemcpyHostToDevice, s));
+      NUS_CUDA(cudaMemcpyAsync(d_mem.ptr, members.data(), d_mem.bytes, cudaMemcpyHostToDevice, s));
+      NUS_CUDA(cudaMemcpyAsync(d_st.ptr, starts.data(), d_st.bytes, cudaMemcpyHostToDevice, s));
+      NUS_CUDA(cudaMemcpyAsync(d_lam.ptr, lam.data(), d_lam.bytes, cudaMemcpyHostToDevice, s));
+      NUS_CUDA(cudaMemcpyAsync(d_ls.ptr, lam_solve.data(), d_ls.bytes, cudaMemcpyHostToDevice, s));
+      cluster_inverse_iteration_kernel<<<static_cast<unsigned>(ncl), kClusterThreads, 0, s>>>(
+          d_diag, d_off, n, d_offs.as<int32_t>(), d_mem.as<int32_t>(), d_st.as<int32_t>(), d_lam.as<double>(),
+          d_ls.as<double>(), anorm, pivmin, d_vec, scr.as<double>());
+      note_launch();
+      check_launch("cluster_inverse_iteration_kernel");
+      NUS_CUDA(cudaStreamSynchronize(s));
+    }
+  }
   DeviceBuffer sg(k * sizeof(double));
   absmax_kernel<<<static_cast<unsigned>(k), 1024, 0, s>>>(d_vec, n, sg.as<double>());
   note_launch();

@@ -1,4 +1,4 @@
-"""GPU: the reference's OWN doctest files (test_nufft.cpp, test_fft.cpp, test_grid.cpp),
+"""GPU: the reference's OWN doctest files (test_nufft.cpp, test_fft.cpp, test_grid.cpp, test_eig.cpp),
 compiled unchanged against include/nuspectral/*.hpp and linked to libnuspectral_b200.so
 (build recipe: `make reftests`; binaries in oracle/_ref/dropin, built where the
 reference tree exists and shipped with the repo snapshot)."""
@@ -13,7 +13,7 @@ pytestmark = pytest.mark.gpu
 DROPIN = os.path.join(ROOT, "oracle", "_ref", "dropin")
 
 
-@pytest.mark.parametrize("name", ["test_nufft", "test_fft", "test_grid"])
+@pytest.mark.parametrize("name", ["test_nufft", "test_fft", "test_grid", "test_eig"])
 def test_reference_doctest_file_passes_against_dropin(name):
     exe = os.path.join(DROPIN, name)
     if not os.path.exists(exe):
