@@ -405,6 +405,27 @@ class REF:
         return p, w, method.value
 
     @staticmethod
+    def run_error_analysis(methods, schemes, trials, base_seed, f_max=0.5, f_w=0.05, k=4, spacing=0.01,
+                           n_samples=50, eps=1e-8):
+        """bench.cpp:130-204 -> list of dicts (scheme-major, method-minor)."""
+        ms = np.ascontiguousarray(methods, np.int32)
+        ss = np.ascontiguousarray(schemes, np.int32)
+        cap = int(round(f_max / spacing)) + 8
+        nrep = ms.size * ss.size
+        cen, mean, sem = np.empty((nrep, cap)), np.empty((nrep, cap)), np.empty((nrep, cap))
+        fl = np.empty((nrep, cap), np.uint8)
+        bands, failed = _i64(0), np.empty(nrep, np.int64)
+        _chk(lib_ref().ref_run_error_analysis(
+            ms.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), _i64(ms.size),
+            ss.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), _i64(ss.size), _i64(trials),
+            ctypes.c_uint64(base_seed), _d(f_max), _d(f_w), _i64(k), _d(spacing), _i64(n_samples), _d(eps),
+            _i64(cap), _p(cen), _p(mean), _p(sem), fl.ctypes.data_as(_u8p), ctypes.byref(bands),
+            failed.ctypes.data_as(_i64p)))
+        b = bands.value
+        return [{"centers": cen[r, :b].copy(), "mean": mean[r, :b].copy(), "sem": sem[r, :b].copy(),
+                 "flags": fl[r, :b].copy(), "failed": int(failed[r])} for r in range(nrep)]
+
+    @staticmethod
     def default_taper_count(tw):
         return int(lib_ref().ref_default_taper_count(tw))
 
@@ -412,6 +433,12 @@ class REF:
     def rng_gauss(seed, count):
         out = np.empty(count)
         _chk(lib_ref().ref_rng_gauss(ctypes.c_uint64(seed), _i64(count), _p(out)))
+        return out
+
+    @staticmethod
+    def rng_uniform(seed, count):
+        out = np.empty(count)
+        _chk(lib_ref().ref_rng_uniform(ctypes.c_uint64(seed), _i64(count), _p(out)))
         return out
 
     @staticmethod

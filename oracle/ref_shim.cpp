@@ -36,6 +36,7 @@
 #include "nuspectral/nufft.hpp"
 #undef private
 
+#include "nuspectral/bench.hpp"
 #include "nuspectral/eig.hpp"
 #include "nuspectral/errors.hpp"
 #include "nuspectral/estimators.hpp"
@@ -467,6 +468,43 @@ int ref_mtnufft0(const double* t, int64_t n, const double* x, double f_max, cons
       for (int64_t j = 0; j < k; ++j)
         for (int64_t i = 0; i < n; ++i) weights[j * n + i] = est.tapers().weights_real(j)[i];
     *method = static_cast<int32_t>(est.method());
+  });
+}
+
+// ---- speed / error harness (bench.cpp:130-275) -------------------------
+
+// run_error_analysis: reports in (scheme-major, method-minor) order; per report the band
+// centres, mse_db_mean, mse_db_sem and flags (bands entries each, NaN where failed)
+int ref_run_error_analysis(const int32_t* methods, int64_t nm, const int32_t* schemes, int64_t ns, int64_t trials,
+                           uint64_t base_seed, double f_max, double f_w, int64_t k, double spacing, int64_t n_samples,
+                           double eps, int64_t cap_bands, double* centers, double* mean, double* sem,
+                           uint8_t* flags, int64_t* bands_out, int64_t* failed_out) {
+  return guard([&] {
+    std::vector<EstimatorMethod> ms;
+    for (int64_t i = 0; i < nm; ++i) ms.push_back(static_cast<EstimatorMethod>(methods[i]));
+    std::vector<SamplingScheme> ss;
+    for (int64_t i = 0; i < ns; ++i) ss.push_back(static_cast<SamplingScheme>(schemes[i]));
+    BenchConfig cfg;
+    cfg.f_max = f_max;
+    cfg.f_w = f_w;
+    cfg.k_tapers = static_cast<size_t>(k);
+    cfg.spacing = spacing;
+    cfg.n_samples = static_cast<size_t>(n_samples);
+    cfg.epsilon = eps;
+    const auto reps = run_error_analysis(ms, ss, static_cast<size_t>(trials), base_seed, cfg);
+    for (size_t r = 0; r < reps.size(); ++r) {
+      const auto& rep = reps[r];
+      const int64_t b = static_cast<int64_t>(rep.centers.size());
+      if (b > cap_bands) throw std::runtime_error("capacity");
+      *bands_out = b;
+      failed_out[r] = static_cast<int64_t>(rep.failed_bands);
+      for (int64_t i = 0; i < b; ++i) {
+        centers[r * cap_bands + i] = rep.centers[i];
+        mean[r * cap_bands + i] = rep.mse_db_mean[i];
+        sem[r * cap_bands + i] = rep.mse_db_sem[i];
+        flags[r * cap_bands + i] = rep.flags[i];
+      }
+    }
   });
 }
 
