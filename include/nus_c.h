@@ -174,6 +174,10 @@ int nus_mtnufft_tapers(nus_mtnufft_t est, double* out_host);
 int nus_mtnufft_setup_ms(nus_mtnufft_t est, double* out5);
 /* estimate(): x [channels][n] fp64 host -> power [channels][I] fp64 host. */
 int nus_mtnufft_estimate(nus_mtnufft_t est, const double* x_host, double* power_host);
+/* estimate() of `steps` series in one call: x [steps][channels][n] -> power [steps][channels][I]
+ * (host, fp64; pinned memory lets the copies run asynchronously).  Copies of one step overlap
+ * the compute of its neighbours (double-buffered device staging, separate H2D / D2H streams). */
+int nus_mtnufft_estimate_batch(nus_mtnufft_t est, const double* x_host, int64_t steps, double* power_host);
 /* eigencoefficients(): -> J [channels][K][I] complex fp64 host (nufft.cpp:194-227). */
 int nus_mtnufft_eigencoefficients(nus_mtnufft_t est, const double* x_host, double* j_host);
 /* Device-resident estimate.  x_dev: [channels][n] of x_dtype (0 f64, 1 f32); power_dev:

@@ -122,6 +122,7 @@ _SIGS = {
     "nus_mtnufft_estimate_device": [_vp, _vp, _i32, _vp, _vp, _vp],
     "nus_mtnufft_spread_device": [_vp, _vp, _i32, _i64, _i64, _vp, _i64, _vp],
     "nus_mtnufft_stage_kernels": [_vp, ctypes.c_char_p, _i64],
+    "nus_mtnufft_estimate_batch": [_vp, _dp, _i64, _dp],
     "nus_generalized_eigen": [_dp, _dp, _dp, _i64, _i64, _d, _d, _i32, _i32, _dp, _dp, _dp],
     "nus_gpss_exact": [_dp, _i64, _d, _d, _d, _i64, _d, _d, _i32, _dp, _dp],
     "nus_band_matrix": [_dp, _i64, _d, _d, _i32, _dp, _dp],

@@ -559,6 +559,13 @@ class _Estimator:
         C.check(C.lib().nus_mtnufft_estimate(self.h, C.dptr(x), C.dptr(out)))
         return out
 
+    def power_batch(self, xs):
+        """[steps][channels][n] -> [steps][channels][I]; copies overlapped across steps."""
+        xs = C.f64(xs).reshape(-1, self.channels, self.n)
+        out = np.empty((xs.shape[0], self.channels, self.nc))
+        C.check(C.lib().nus_mtnufft_estimate_batch(self.h, C.dptr(xs), xs.shape[0], C.dptr(out)))
+        return out
+
     def f_test(self, x, cap=1e12):
         x = C.f64(x).reshape(self.channels, self.n)
         f = np.empty((self.channels, self.nc))
@@ -636,6 +643,17 @@ class MtnufftEstimator:
             raise InvalidArgument("SpectrumEstimate: negative power")
         return SpectrumEstimate(self._plan, p, self._method, np.full(bands, self._opts.k_tapers),
                                 np.full(bands, self._plan.half_width()), self._plan.flags())
+
+    def estimate_many(self, series) -> List[SpectrumEstimate]:
+        """estimate() of many series on this grid in one pipelined call (the H2D / D2H copies of
+        one series overlap the compute of its neighbours).  Same results as estimate() each."""
+        v = np.asarray(series, dtype=np.float64)
+        if v.ndim != 2 or v.shape[1] != self._grid.n_samples():
+            raise InvalidArgument("estimate_many: expected [series][n_samples] values")
+        p = self._est.power_batch(v)
+        bands = self._plan.size()
+        return [SpectrumEstimate(self._plan, p[i, 0], self._method, np.full(bands, self._opts.k_tapers),
+                                 np.full(bands, self._plan.half_width()), self._plan.flags()) for i in range(len(v))]
 
     def eigencoefficients(self, values) -> EigenCoefficients:
         j = self._est.eigencoefficients(values)[0]

@@ -481,6 +481,14 @@ int nus_mtnufft_estimate(nus_mtnufft_t est, const double* x_host, double* power_
   });
 }
 
+int nus_mtnufft_estimate_batch(nus_mtnufft_t est, const double* x_host, int64_t steps, double* power_host) {
+  return guarded([&] {
+    nus::require(est && x_host && power_host, "estimate_batch: null argument");
+    nus::require(steps >= 1, "estimate_batch: steps must be >= 1");
+    nus::estimator_estimate_batch_host(*est->est, x_host, steps, power_host);
+  });
+}
+
 int nus_mtnufft_eigencoefficients(nus_mtnufft_t est, const double* x_host, double* j_host) {
   return guarded([&] {
     nus::require(est && x_host && j_host, "eigencoefficients: null argument");

@@ -218,6 +218,47 @@ void estimator_estimate_host(Estimator& est, const double* x, double* power, dou
   NUS_CUDA(cudaStreamSynchronize(s));
 }
 
+// Pipelined host estimate of `steps` series (x [steps][C][n], power [steps][C][I], host):
+// step s's H2D copy, compute and D2H copy run on three streams with double-buffered device
+// staging, so the copies of one step overlap the compute of its neighbours (copy engines in
+// both directions at once).  Every step still moves its own input in and its own P out.
+void estimator_estimate_batch_host(Estimator& est, const double* x, int64_t steps, double* power) {
+  std::lock_guard<std::mutex> lock(est.mu);
+  use_device(est.cfg.device);
+  const PlanParams& p = est.plan->p;
+  const int64_t C = est.cfg.channels, n = est.cfg.n;
+  const size_t xbytes = static_cast<size_t>(C) * n * sizeof(double), pbytes = static_cast<size_t>(C) * p.nc * sizeof(double);
+  cudaStream_t cs = est.stream();
+  if (!est.h2d) {
+    NUS_CUDA(cudaStreamCreateWithFlags(&est.h2d, cudaStreamNonBlocking));
+    NUS_CUDA(cudaStreamCreateWithFlags(&est.d2h, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+      NUS_CUDA(cudaEventCreateWithFlags(&est.ev_x[b], cudaEventDisableTiming));
+      NUS_CUDA(cudaEventCreateWithFlags(&est.ev_c[b], cudaEventDisableTiming));
+      NUS_CUDA(cudaEventCreateWithFlags(&est.ev_p[b], cudaEventDisableTiming));
+    }
+  }
+  for (int b = 0; b < 2; ++b) {
+    if (est.xb[b].bytes < xbytes) est.xb[b].alloc(xbytes);
+    if (est.pb[b].bytes < pbytes) est.pb[b].alloc(pbytes);
+  }
+  for (int64_t st = 0; st < steps; ++st) {
+    const int b = static_cast<int>(st & 1);
+    if (st >= 2) NUS_CUDA(cudaStreamWaitEvent(est.h2d, est.ev_c[b], 0));  // x buffer consumed
+    NUS_CUDA(cudaMemcpyAsync(est.xb[b].ptr, x + st * C * n, xbytes, cudaMemcpyHostToDevice, est.h2d));
+    NUS_CUDA(cudaEventRecord(est.ev_x[b], est.h2d));
+    NUS_CUDA(cudaStreamWaitEvent(cs, est.ev_x[b], 0));
+    if (st >= 2) NUS_CUDA(cudaStreamWaitEvent(cs, est.ev_p[b], 0));  // P buffer drained
+    estimator_run(est, est.xb[b].ptr, 0, est.pb[b].ptr, true, nullptr, cs);
+    NUS_CUDA(cudaEventRecord(est.ev_c[b], cs));
+    NUS_CUDA(cudaStreamWaitEvent(est.d2h, est.ev_c[b], 0));
+    NUS_CUDA(cudaMemcpyAsync(power + st * C * p.nc, est.pb[b].ptr, pbytes, cudaMemcpyDeviceToHost, est.d2h));
+    NUS_CUDA(cudaEventRecord(est.ev_p[b], est.d2h));
+  }
+  NUS_CUDA(cudaStreamSynchronize(est.d2h));
+  NUS_CUDA(cudaStreamSynchronize(cs));
+}
+
 void estimator_timing_enable(Estimator& est, size_t max_runs) {
   for (auto e : est.tev) cudaEventDestroy(e);
   est.tev.assign(4 * max_runs, nullptr);
@@ -247,6 +288,13 @@ cudaStream_t Estimator::stream() {
 
 Estimator::~Estimator() {
   for (auto e : tev) cudaEventDestroy(e);
+  for (int b = 0; b < 2; ++b) {
+    if (ev_x[b]) cudaEventDestroy(ev_x[b]);
+    if (ev_c[b]) cudaEventDestroy(ev_c[b]);
+    if (ev_p[b]) cudaEventDestroy(ev_p[b]);
+  }
+  if (h2d) cudaStreamDestroy(h2d);
+  if (d2h) cudaStreamDestroy(d2h);
   if (own_stream) cudaStreamDestroy(own_stream);
 }
 

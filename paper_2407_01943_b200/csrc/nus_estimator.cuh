@@ -12,6 +12,10 @@ struct Estimator {
   DeviceBuffer tapers_sorted;  // plan precision [C][K][n], start-cell order
   DeviceBuffer grid;           // [C][K][Mr] complex, plan precision
   DeviceBuffer x_stage, p_stage, j_stage;  // host-API staging
+  // estimate_batch: double-buffered staging and the copy streams / events of the pipeline
+  DeviceBuffer xb[2], pb[2];
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t ev_x[2] = {nullptr, nullptr}, ev_c[2] = {nullptr, nullptr}, ev_p[2] = {nullptr, nullptr};
   double setup_ms[5] = {0, 0, 0, 0, 0};
   std::mutex mu;
   cudaStream_t own_stream = nullptr;
@@ -28,6 +32,7 @@ std::unique_ptr<Estimator> estimator_create(const nus_mtnufft_config_t& cfg, con
                                             const double* centers, const double* tapers);
 void estimator_run(Estimator& est, const void* x_dev, int x_dtype, void* power_dev, bool power_f64,
                    void* j_dev, cudaStream_t s);
+void estimator_estimate_batch_host(Estimator& est, const double* x, int64_t steps, double* power);
 void estimator_estimate_host(Estimator& est, const double* x, double* power, double* j);
 void estimator_timing_enable(Estimator& est, size_t max_runs);
 void estimator_timing_read(Estimator& est, double* ms3, int64_t* runs);

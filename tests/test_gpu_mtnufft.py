@@ -174,3 +174,13 @@ def test_estimate_mtnufft_one_shot_matches_estimator():
     a = nus.estimate_mtnufft(series, nus.SignalBand(wl.f_max), plan, 3, 1e-9).power
     b = estimator(wl, k=3).estimate(wl.values).power
     assert rel_l2(a, b) < 1e-14
+
+
+def test_estimate_many_equals_estimate(c2_case):
+    """The pipelined batch entry (copies overlapped across steps) returns exactly estimate()'s P."""
+    wl, est, _, _ = c2_case
+    xs = np.stack([np.roll(wl.values, 101 * i) for i in range(5)])
+    many = est.estimate_many(xs)
+    assert len(many) == 5
+    for i in (0, 3, 4):
+        assert np.array_equal(many[i].power, est.estimate(xs[i]).power)
