@@ -26,18 +26,45 @@ namespace {
 
 // ---------------------------------------------------------------- Sturm counts
 
-// Each thread evaluates kProbes shift values (independent chains give ILP).
+// Each thread evaluates kProbes shift values (independent chains give ILP).  The quotient
+// e_i^2 / q uses a branch-free reciprocal (MUFU seed + two Newton steps, <= 1 ulp): the IEEE
+// divide's slow-path branch would otherwise serialise the kProbes chains (613 vs ~150 cycles
+// per row, scratch microbenchmark).  All threads of a block walk the same rows, so d and e^2
+// are staged through shared memory a chunk ahead with cp.async.
 constexpr int kProbes = 4;
 constexpr int kSturmThreads = 64;
+constexpr int kSturmChunk = 1024;
 
-__global__ void sturm_multisect_kernel(const double* __restrict__ d, const double* __restrict__ e2,
-                                       int64_t n, const double* __restrict__ lo,
-                                       const double* __restrict__ hi, int probes_per_eig,
-                                       double pivmin, int32_t* __restrict__ counts) {
+__device__ inline double rcp_nr2(double b) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(b));
+  double e = fma(-b, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-b, r, 1.0);
+  return fma(r, e, r);
+}
+
+__device__ inline void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ inline void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ inline void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ inline void cp_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+__global__ void __launch_bounds__(kSturmThreads) sturm_multisect_kernel(
+    const double* __restrict__ d, const double* __restrict__ e2, int64_t n, const double* __restrict__ lo,
+    const double* __restrict__ hi, int probes_per_eig, double pivmin, int32_t* __restrict__ counts) {
+  constexpr int CH = kSturmChunk;
+  __shared__ double sd[2][CH], se[2][CH];
   const int j = blockIdx.y;  // eigenvalue rank
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const int p0 = t * kProbes;
-  if (p0 >= probes_per_eig) return;
   const double a = lo[j], b = hi[j];
   const double step = (b - a) / static_cast<double>(probes_per_eig + 1);
   double lam[kProbes], q[kProbes];
@@ -49,15 +76,35 @@ __global__ void sturm_multisect_kernel(const double* __restrict__ d, const doubl
     if (fabs(q[u]) < pivmin) q[u] = -pivmin;
     cnt[u] = q[u] < 0.0 ? 1 : 0;
   }
-  for (int64_t i = 1; i < n; ++i) {
-    const double di = d[i], ei = e2[i - 1];
-#pragma unroll
-    for (int u = 0; u < kProbes; ++u) {
-      double v = (di - lam[u]) - ei / q[u];
-      if (fabs(v) < pivmin) v = -pivmin;
-      q[u] = v;
-      cnt[u] += v < 0.0 ? 1 : 0;
+  // rows i = 1 .. n-1; chunk c holds i in [1 + c CH, 1 + c CH + CH)
+  const int64_t rows = n - 1, nch = (rows + CH - 1) / CH;
+  auto load = [&](int64_t c, int buf) {
+    const int64_t i0 = 1 + c * CH, cnt_c = rows - c * CH < CH ? rows - c * CH : static_cast<int64_t>(CH);
+    for (int r = threadIdx.x; r < cnt_c; r += kSturmThreads) {
+      cp_async8(&sd[buf][r], d + i0 + r);
+      cp_async8(&se[buf][r], e2 + i0 + r - 1);
     }
+    cp_commit();
+  };
+  if (nch > 0) load(0, 0);
+  for (int64_t c = 0; c < nch; ++c) {
+    const int buf = static_cast<int>(c & 1);
+    if (c + 1 < nch) load(c + 1, buf ^ 1);
+    else cp_commit();
+    cp_wait1();
+    __syncthreads();
+    const int cnt_c = static_cast<int>(rows - c * CH < CH ? rows - c * CH : CH);
+    for (int r = 0; r < cnt_c; ++r) {
+      const double di = sd[buf][r], ei = se[buf][r];
+#pragma unroll
+      for (int u = 0; u < kProbes; ++u) {
+        double v = (di - lam[u]) - ei * rcp_nr2(q[u]);
+        if (fabs(v) < pivmin) v = -pivmin;
+        q[u] = v;
+        cnt[u] += v < 0.0 ? 1 : 0;
+      }
+    }
+    __syncthreads();
   }
 #pragma unroll
   for (int u = 0; u < kProbes; ++u)
@@ -71,9 +118,6 @@ __global__ void square_kernel(const double* __restrict__ e, int64_t m, double* _
 
 // ------------------------------------------------- inverse iteration (double-double)
 
-// L1 prefetch hint: the sequential sweeps below walk arrays one element per step; pulling
-// lines into L1 a few hundred bytes ahead turns ~600-cycle DRAM round trips into L1 hits.
-__device__ inline void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 
 __device__ inline uint64_t mix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -81,118 +125,173 @@ __device__ inline uint64_t mix64(uint64_t z) {
   return z ^ (z >> 31);
 }
 
-// One thread per eigenvector.  Each iteration solves (T - sigma I) x_new = x
-// with partial pivoting (the structure of src/eig.cpp:119-168) entirely in
-// double-double, storing the U factor rows (inverse pivot, u1, u2) in global
-// scratch for the back substitution.  x is renormalised between iterations.
-__global__ void inverse_iteration_dd_kernel(const double* __restrict__ d, const double* __restrict__ e,
-                                            int64_t n, const double* __restrict__ sigma_hi,
-                                            const double* __restrict__ sigma_lo, int iters,
-                                            double pivmin, dd* __restrict__ xs, dd* __restrict__ us,
-                                            double* __restrict__ norms) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= gridDim.x * blockDim.x) return;
-  const int64_t k_count = gridDim.x * blockDim.x;
-  (void)k_count;
+// Inverse iteration, one warp per eigenvector.  Each iteration solves (T - sigma I) x_new = x
+// with partial pivoting (the structure of src/eig.cpp:119-168) entirely in double-double,
+// storing the U factor rows (inverse pivot, u1, u2) in global scratch for the back
+// substitution; x is renormalised between iterations.
+// The recurrences stay serial on lane 0, but every input row
+// (d, e, x forward; x, U backward) is brought into shared memory by cp.async one chunk ahead
+// and every output row leaves through coalesced stores by the whole warp, so lane 0 never
+// waits on a dependent global load (the one-thread version was global-latency bound).
+constexpr int kIiChunk = 128;
+
+
+__global__ void ii_init_kernel(dd* __restrict__ xs, int64_t n, int k) {
+  const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (g >= n * k) return;
+  const int64_t j = g / n, i = g - j * n;  // same pseudo-random start as the one-thread kernel
+  const uint64_t r = mix64(0x9E3779B97F4A7C15ull * static_cast<uint64_t>(j + 1) + static_cast<uint64_t>(i));
+  xs[g] = dd{static_cast<double>(r >> 11) * 0x1.0p-53 - 0.5, 0.0};
+}
+
+__global__ void __launch_bounds__(32) inverse_iteration_dd_warp_kernel(
+    const double* __restrict__ d, const double* __restrict__ e, int64_t n, const double* __restrict__ sigma_hi,
+    const double* __restrict__ sigma_lo, int iters, double pivmin, dd* __restrict__ xs, dd* __restrict__ us,
+    double* __restrict__ norms) {
+  constexpr int CH = kIiChunk;
+  __shared__ double sd[2][CH], se[2][CH + 1];
+  __shared__ dd sx[2][CH];
+  __shared__ dd ox[CH], ou[3 * CH], su[2][3 * CH];
+  const int j = blockIdx.x, lane = threadIdx.x;
   dd* x = xs + static_cast<int64_t>(j) * n;
-  dd* u = us + static_cast<int64_t>(j) * n * 3;  // per row: inv u0, u1, u2
+  dd* u = us + static_cast<int64_t>(j) * n * 3;
   const dd sig = {sigma_hi[j], sigma_lo[j]};
-  // pseudo-random start vector in [-0.5, 0.5)
-  for (int64_t i = 0; i < n; ++i) {
-    const uint64_t r = mix64(0x9E3779B97F4A7C15ull * static_cast<uint64_t>(j + 1) + static_cast<uint64_t>(i));
-    x[i] = dd{static_cast<double>(r >> 11) * 0x1.0p-53 - 0.5, 0.0};
-  }
-  dd scale = {1.0, 0.0};
   const dd pm = {pivmin, 0.0};
-  double final_norm = 1.0;
-  for (int it = 0; it < iters; ++it) {
-    if (n == 1) {
+  dd scale = {1.0, 0.0};
+  if (n == 1) {
+    if (lane == 0) {
       dd p = dd_sub(dd_from(d[0]), sig);
       if (fabs(p.hi) < pivmin) p = p.hi < 0 ? dd_neg(pm) : pm;
-      x[0] = dd_div(dd_mul(x[0], scale), p);
-      final_norm = fabs(x[0].hi);
-      scale = dd_div(dd_from(1.0), dd_from(final_norm));
-      break;
+      x[0] = dd_mul(x[0], dd_recip(p));
+      const dd sc = dd_recip(dd_from(fabs(x[0].hi)));
+      norms[2 * j] = sc.hi;
+      norms[2 * j + 1] = sc.lo;
     }
-    // forward elimination
-    dd c0 = dd_sub(dd_from(d[0]), sig);
-    dd c1 = dd_from(e[0]);
-    dd c2 = dd_from(0.0);
-    dd xi = dd_mul(x[0], scale);
-    for (int64_t i = 0; i + 1 < n; ++i) {
-      if ((i & 3) == 0 && i + 96 < n) {
-        prefetch_l1(d + i + 96);
-        prefetch_l1(e + i + 96);
-        prefetch_l1(x + i + 48);
-      }
-      const double sub = e[i];
-      const dd ddv = dd_sub(dd_from(d[i + 1]), sig);
-      const double sup = (i + 2 < n) ? e[i + 1] : 0.0;
-      dd xn = dd_mul(x[i + 1], scale);
-      if (fabs(sub) > fabs(c0.hi)) {
-        // pivot on the row below: row i <- (sub, dd, sup), swap rhs
-        const dd m = dd_div(c0, dd_from(sub));
-        u[3 * i] = dd_div(dd_from(1.0), dd_from(sub));
-        u[3 * i + 1] = ddv;
-        u[3 * i + 2] = dd_from(sup);
-        const dd tmp = xi;
-        x[i] = xn;
-        xi = dd_sub(tmp, dd_mul(m, xn));
-        c0 = dd_sub(c1, dd_mul(m, ddv));
-        c1 = dd_sub(c2, dd_mul_d(m, sup));
-        c2 = dd_from(0.0);
-      } else {
-        if (fabs(c0.hi) < pivmin) c0 = c0.hi < 0 ? dd_neg(pm) : pm;
-        const dd inv = dd_div(dd_from(1.0), c0);
-        u[3 * i] = inv;
-        u[3 * i + 1] = c1;
-        u[3 * i + 2] = c2;
-        x[i] = xi;
-        const dd m = dd_mul_d(inv, sub);
-        xi = dd_sub(xn, dd_mul(m, xi));
-        c0 = dd_sub(ddv, dd_mul(m, c1));
-        c1 = dd_sub(dd_from(sup), dd_mul(m, c2));
-        c2 = dd_from(0.0);
-      }
-    }
-    if (fabs(c0.hi) < pivmin) c0 = c0.hi < 0 ? dd_neg(pm) : pm;
-    // back substitution
-    dd xl = dd_div(xi, c0);
-    x[n - 1] = xl;
-    dd nrm = dd_mul(xl, xl);
-    dd xl1 = xl;  // x[i+1]
-    dd xl2 = dd_from(0.0);  // x[i+2]
-    {
-      const int64_t i = n - 2;
-      const dd v = dd_mul(dd_sub(x[i], dd_mul(u[3 * i + 1], xl1)), u[3 * i]);
-      x[i] = v;
-      nrm = dd_add(nrm, dd_mul(v, v));
-      xl2 = xl1;
-      xl1 = v;
-    }
-    for (int64_t i = n - 2; i-- > 0;) {
-      if ((i & 3) == 0 && i >= 48) {
-        prefetch_l1(x + i - 48);
-        prefetch_l1(u + 3 * (i - 16));
-        prefetch_l1(u + 3 * (i - 20));
-        prefetch_l1(u + 3 * (i - 24));
-      }
-      const dd r = dd_sub(dd_sub(x[i], dd_mul(u[3 * i + 1], xl1)), dd_mul(u[3 * i + 2], xl2));
-      const dd v = dd_mul(r, u[3 * i]);
-      x[i] = v;
-      nrm = dd_add(nrm, dd_mul(v, v));
-      xl2 = xl1;
-      xl1 = v;
-    }
-    final_norm = sqrt(nrm.hi);
-    // scale = 1/sqrt(nrm) in dd (one Newton step on the fp64 estimate)
-    const double s0 = 1.0 / final_norm;
-    const dd s0d = dd_from(s0);
-    const dd resid = dd_sub(dd_from(1.0), dd_mul(nrm, dd_mul(s0d, s0d)));
-    scale = dd_add(s0d, dd_mul_d(dd_mul_d(resid, s0), 0.5));
+    return;
   }
-  norms[2 * j] = scale.hi;
-  norms[2 * j + 1] = scale.lo;
+  const int64_t rows = n - 1;  // forward elimination rows i = 0 .. n-2
+  const int64_t nch = (rows + CH - 1) / CH;
+  for (int it = 0; it < iters; ++it) {
+    // ---- forward elimination: chunk c holds rows [c CH, c CH + CH) with inputs
+    // d[i+1], e[i], e[i+1] (sup), x[i+1]; outputs x[i], U row i
+    auto load_fwd = [&](int64_t c, int b) {
+      const int64_t i0 = c * CH, cnt = rows - i0 < CH ? rows - i0 : static_cast<int64_t>(CH);
+      for (int q = lane; q < cnt; q += 32) {
+        cp_async8(&sd[b][q], d + i0 + q + 1);
+        cp_async16(&sx[b][q], x + i0 + q + 1);
+      }
+      for (int q = lane; q <= cnt; q += 32)
+        if (i0 + q < rows) cp_async8(&se[b][q], e + i0 + q);
+      cp_commit();
+    };
+    dd c0 = dd_sub(dd_from(d[0]), sig), c1 = dd_from(e[0]), c2 = dd_from(0.0);
+    dd xi = dd_mul(x[0], scale);
+    load_fwd(0, 0);
+    for (int64_t c = 0; c < nch; ++c) {
+      const int b = static_cast<int>(c & 1);
+      if (c + 1 < nch) load_fwd(c + 1, b ^ 1);
+      else cp_commit();
+      cp_wait1();
+      __syncwarp();
+      const int64_t i0 = c * CH, cnt = rows - i0 < CH ? rows - i0 : static_cast<int64_t>(CH);
+      if (lane == 0) {
+        for (int q = 0; q < cnt; ++q) {
+          const int64_t i = i0 + q;
+          const double sub = se[b][q];
+          const dd ddv = dd_sub(dd_from(sd[b][q]), sig);
+          const double sup = (i + 2 < n) ? se[b][q + 1] : 0.0;
+          const dd xn = dd_mul(sx[b][q], scale);
+          if (fabs(sub) > fabs(c0.hi)) {
+            // pivot on the row below: row i <- (sub, dd, sup), swap rhs
+            const dd isub = dd_recip(dd_from(sub));
+            const dd m = dd_mul(c0, isub);
+            ou[3 * q] = isub;
+            ou[3 * q + 1] = ddv;
+            ou[3 * q + 2] = dd_from(sup);
+            const dd tmp = xi;
+            ox[q] = xn;
+            xi = dd_sub(tmp, dd_mul(m, xn));
+            c0 = dd_sub(c1, dd_mul(m, ddv));
+            c1 = dd_sub(c2, dd_mul_d(m, sup));
+            c2 = dd_from(0.0);
+          } else {
+            if (fabs(c0.hi) < pivmin) c0 = c0.hi < 0 ? dd_neg(pm) : pm;
+            const dd inv = dd_recip(c0);
+            ou[3 * q] = inv;
+            ou[3 * q + 1] = c1;
+            ou[3 * q + 2] = c2;
+            ox[q] = xi;
+            const dd m = dd_mul_d(inv, sub);
+            xi = dd_sub(xn, dd_mul(m, xi));
+            c0 = dd_sub(ddv, dd_mul(m, c1));
+            c1 = dd_sub(dd_from(sup), dd_mul(m, c2));
+            c2 = dd_from(0.0);
+          }
+        }
+      }
+      __syncwarp();
+      for (int q = lane; q < cnt; q += 32) x[i0 + q] = ox[q];
+      for (int q = lane; q < 3 * cnt; q += 32) u[3 * i0 + q] = ou[q];
+      __syncwarp();
+    }
+    // the last pivot and x[n-1], broadcast from lane 0
+    if (lane == 0) {
+      if (fabs(c0.hi) < pivmin) c0 = c0.hi < 0 ? dd_neg(pm) : pm;
+      x[n - 1] = dd_mul(xi, dd_recip(c0));
+    }
+    __threadfence_block();
+    __syncwarp();
+    // ---- back substitution, chunks from the top: rows [c CH, c CH + CH), i descending;
+    // the chunk below is prefetched (x rows and U rows) while lane 0 works on this one
+    auto load_bwd = [&](int64_t c, int b) {
+      const int64_t i0 = c * CH, cnt = rows - i0 < CH ? rows - i0 : static_cast<int64_t>(CH);
+      for (int q = lane; q < cnt; q += 32) cp_async16(&sx[b][q], x + i0 + q);
+      for (int q = lane; q < 3 * cnt; q += 32) cp_async16(&su[b][q], u + 3 * i0 + q);
+      cp_commit();
+    };
+    dd xl1 = x[n - 1], xl2 = dd_from(0.0);
+    dd nrm = dd_mul(xl1, xl1);
+    load_bwd(nch - 1, 0);
+    for (int64_t cc = 0; cc < nch; ++cc) {
+      const int64_t c = nch - 1 - cc;
+      const int b = static_cast<int>(cc & 1);
+      if (cc + 1 < nch) load_bwd(c - 1, b ^ 1);
+      else cp_commit();
+      cp_wait1();
+      __syncwarp();
+      const int64_t i0 = c * CH, cnt = rows - i0 < CH ? rows - i0 : static_cast<int64_t>(CH);
+      if (lane == 0) {
+        for (int q = static_cast<int>(cnt) - 1; q >= 0; --q) {
+          const int64_t i = i0 + q;
+          // x_i - u2 x_{i+2} is off the loop-carried path; only u1 x_{i+1} waits on the last row
+          const dd t = i != n - 2 ? dd_sub(sx[b][q], dd_mul(su[b][3 * q + 2], xl2)) : sx[b][q];
+          const dd v = dd_mul(dd_sub(t, dd_mul(su[b][3 * q + 1], xl1)), su[b][3 * q]);
+          ox[q] = v;
+          nrm = dd_add(nrm, dd_mul(v, v));
+          xl2 = xl1;
+          xl1 = v;
+        }
+      }
+      __syncwarp();
+      for (int q = lane; q < cnt; q += 32) x[i0 + q] = ox[q];
+      __syncwarp();
+    }
+    if (lane == 0) {
+      const double fn = sqrt(nrm.hi);
+      const double s0 = 1.0 / fn;
+      const dd s0d = dd_from(s0);
+      const dd resid = dd_sub(dd_from(1.0), dd_mul(nrm, dd_mul(s0d, s0d)));
+      scale = dd_add(s0d, dd_mul_d(dd_mul_d(resid, s0), 0.5));
+    }
+    scale.hi = __shfl_sync(0xffffffffu, scale.hi, 0);
+    scale.lo = __shfl_sync(0xffffffffu, scale.lo, 0);
+    __threadfence_block();
+    __syncwarp();
+  }
+  if (lane == 0) {
+    norms[2 * j] = scale.hi;
+    norms[2 * j + 1] = scale.lo;
+  }
 }
 
 // out[j][i] = x_j[i] * scale_j  (dd -> fp64)
@@ -675,6 +774,15 @@ __global__ void cluster_inverse_iteration_kernel(const double* __restrict__ d, c
 DpssResult tridiag_top_device(const double* d_diag, const double* d_off, int64_t n, int64_t k,
                               double* d_vec, cudaStream_t s) {
   require(k >= 1 && k <= n, "tridiagonal_eigen: k_top out of range");
+  const bool prof = std::getenv("NUS_DPSS_PROF") != nullptr;
+  auto tic = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!prof) return;
+    NUS_CUDA(cudaStreamSynchronize(s));
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[dpss] %s %.3f s\n", what, std::chrono::duration<double>(now - tic).count());
+    tic = now;
+  };
   // Gershgorin bounds and ||T||_inf from host copies (O(n) validation work)
   std::vector<double> hd(n), he(n > 1 ? n - 1 : 0);
   NUS_CUDA(cudaMemcpyAsync(hd.data(), d_diag, n * sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -711,6 +819,7 @@ DpssResult tridiag_top_device(const double* d_diag, const double* d_off, int64_t
     bool done = true;
     for (int64_t j = 0; j < k; ++j) done = done && (hi[j] - lo[j] <= target);
     if (done) break;
+    if (prof) std::fprintf(stderr, "[dpss] sturm pass %d\n", pass);
     NUS_CUDA(cudaMemcpyAsync(d_lo.ptr, lo.data(), k * sizeof(double), cudaMemcpyHostToDevice, s));
     NUS_CUDA(cudaMemcpyAsync(d_hi.ptr, hi.data(), k * sizeof(double), cudaMemcpyHostToDevice, s));
     const dim3 grid(blocks_for(probes / kProbes, kSturmThreads), static_cast<unsigned>(k));
@@ -736,6 +845,7 @@ DpssResult tridiag_top_device(const double* d_diag, const double* d_off, int64_t
       hi[j] = nhi;
     }
   }
+  lap("gershgorin+sturm");
   DpssResult res;
   res.values.resize(k);
   std::vector<double> sig_hi(k), sig_lo(k);
@@ -763,11 +873,14 @@ DpssResult tridiag_top_device(const double* d_diag, const double* d_off, int64_t
   DeviceBuffer xs(static_cast<size_t>(k) * n * sizeof(dd)), us(static_cast<size_t>(k) * n * 3 * sizeof(dd));
   NUS_CUDA(cudaMemcpyAsync(d_sh.ptr, sig_hi.data(), k * sizeof(double), cudaMemcpyHostToDevice, s));
   NUS_CUDA(cudaMemcpyAsync(d_sl.ptr, sig_lo.data(), k * sizeof(double), cudaMemcpyHostToDevice, s));
-  inverse_iteration_dd_kernel<<<static_cast<unsigned>(k), 1, 0, s>>>(
+  ii_init_kernel<<<blocks_for(n * k, 256), 256, 0, s>>>(xs.as<dd>(), n, static_cast<int>(k));
+  note_launch();
+  inverse_iteration_dd_warp_kernel<<<static_cast<unsigned>(k), 32, 0, s>>>(
       d_diag, d_off, n, d_sh.as<double>(), d_sl.as<double>(), 3, pivmin, xs.as<dd>(), us.as<dd>(),
       d_norm.as<double>());
   note_launch();
-  check_launch("inverse_iteration_dd_kernel");
+  check_launch("inverse_iteration_dd_warp_kernel");
+  lap("inverse iteration");
   dd_finalize_kernel<<<blocks_for(n * k, 256), 256, 0, s>>>(xs.as<dd>(), d_norm.as<double>(), n,
                                                             static_cast<int>(k), d_vec);
   note_launch();
@@ -838,6 +951,7 @@ DpssResult tridiag_top_device(const double* d_diag, const double* d_off, int64_t
       NUS_CUDA(cudaStreamSynchronize(s));
     }
   }
+  lap("clusters");
   DeviceBuffer sg(k * sizeof(double));
   absmax_kernel<<<static_cast<unsigned>(k), 1024, 0, s>>>(d_vec, n, sg.as<double>());
   note_launch();
