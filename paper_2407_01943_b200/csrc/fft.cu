@@ -272,6 +272,9 @@ __global__ void __launch_bounds__(kFftThreads, 2) fft_cols_kernel(
 
 // ---- pass B + crop / power ---------------------------------------------------------------
 
+constexpr int kCropN = 9;  // last-stage outputs q the crop can keep (pass B, Mr >= 2 nc)
+__host__ __device__ constexpr int crop_q(int c) { return c < 5 ? c : c + 7; }
+
 template <typename Real, typename PReal, int R0>
 __global__ void __launch_bounds__(kFftThreads, 2) fft_rows_crop_kernel(
     const typename C2<Real>::T* __restrict__ grid, int64_t mr, int R, int C, int RPC, int64_t kpad,
@@ -284,9 +287,11 @@ __global__ void __launch_bounds__(kFftThreads, 2) fft_rows_crop_kernel(
   const int k1 = blockIdx.x;                        // one row per CTA
   const int64_t ch = blockIdx.y;
   const int lgC = __ffs(C) - 1;
-  Real acc[16];
+  // Mr >= 2 nc, so the crop keeps k2 <= C/4 or k2 >= 3C/4 only: of this thread's outputs
+  // k2 = out0 + q C/16 that is q in {0..4, 12..15} (kCropQ); the other seven are never formed
+  Real acc[kCropN];
 #pragma unroll
-  for (int q = 0; q < 16; ++q) acc[q] = Real(0);
+  for (int c = 0; c < kCropN; ++c) acc[c] = Real(0);
   int f = 0, out0 = 0, step = 1;
   for (int kk = 0; kk < k_count; ++kk) {
     const T2* g = grid + (ch * kpad + kk) * mr + static_cast<int64_t>(k1) * C;
@@ -299,9 +304,10 @@ __global__ void __launch_bounds__(kFftThreads, 2) fft_rows_crop_kernel(
     }
     fft16_regs<R0, true>(v, buf, lgC, 0, 1, C, tw_c, f, out0, step);
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {
+    for (int c = 0; c < kCropN; ++c) {
+      const int q = crop_q(c);
       const T2 x = v[q];
-      acc[q] += x.x * x.x + x.y * x.y;
+      acc[c] += x.x * x.x + x.y * x.y;
       if (j_out) {
         const int64_t k = static_cast<int64_t>(k1) + static_cast<int64_t>(R) * (out0 + q * step);
         int64_t i = -1;
@@ -318,14 +324,15 @@ __global__ void __launch_bounds__(kFftThreads, 2) fft_rows_crop_kernel(
   if (!power) return;
   // crop (nufft.cpp:131-140): bin k = k1 + R k2 keeps i = m + I/2 for m in [-I/2, I - I/2), (-m) mod Mr = k
 #pragma unroll
-  for (int q = 0; q < 16; ++q) {
+  for (int c = 0; c < kCropN; ++c) {
+    const int q = crop_q(c);
     const int64_t k = static_cast<int64_t>(k1) + static_cast<int64_t>(R) * (out0 + q * step);
     int64_t i = -1;
     if (k <= mode_offset) i = mode_offset - k;
     else if (mr - k < nc - mode_offset) i = mode_offset + (mr - k);
     if (i >= 0 && i < nc) {
       const double d = static_cast<double>(deconv[i]);
-      const PReal val = static_cast<PReal>(d * d * static_cast<double>(acc[q]) / divisor);
+      const PReal val = static_cast<PReal>(d * d * static_cast<double>(acc[c]) / divisor);
       PReal* dst = power + ch * nc + i;
       *dst = accumulate ? *dst + val : val;
     }
