@@ -322,16 +322,25 @@ __global__ void __launch_bounds__(kFftThreads, 2) fft_rows_crop_kernel(
     __syncthreads();  // buf reused by the next taper
   }
   if (!power) return;
-  // crop (nufft.cpp:131-140): bin k = k1 + R k2 keeps i = m + I/2 for m in [-I/2, I - I/2), (-m) mod Mr = k
+  // crop (nufft.cpp:131-140): bin k = k1 + R k2 keeps i = m + I/2 for m in [-I/2, I - I/2), (-m) mod Mr = k.
+  // All nine deconvolution factors are loaded (clamped index) before the first is used, so their
+  // latencies overlap instead of queueing behind nine branches.
+  int64_t iv[kCropN];
+  Real dv[kCropN];
 #pragma unroll
   for (int c = 0; c < kCropN; ++c) {
-    const int q = crop_q(c);
-    const int64_t k = static_cast<int64_t>(k1) + static_cast<int64_t>(R) * (out0 + q * step);
+    const int64_t k = static_cast<int64_t>(k1) + static_cast<int64_t>(R) * (out0 + crop_q(c) * step);
     int64_t i = -1;
     if (k <= mode_offset) i = mode_offset - k;
     else if (mr - k < nc - mode_offset) i = mode_offset + (mr - k);
+    iv[c] = i;
+    dv[c] = deconv[i < 0 ? 0 : (i < nc ? i : nc - 1)];
+  }
+#pragma unroll
+  for (int c = 0; c < kCropN; ++c) {
+    const int64_t i = iv[c];
     if (i >= 0 && i < nc) {
-      const double d = static_cast<double>(deconv[i]);
+      const double d = static_cast<double>(dv[c]);
       const PReal val = static_cast<PReal>(d * d * static_cast<double>(acc[c]) / divisor);
       PReal* dst = power + ch * nc + i;
       *dst = accumulate ? *dst + val : val;
