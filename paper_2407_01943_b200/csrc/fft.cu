@@ -470,17 +470,21 @@ __global__ void __launch_bounds__(kFftThreads * kGroups, 1) fft_cols_async_kerne
                       CW, row_lo, row_cnt, &bars[b]);
   }
   __syncthreads();
-  for (int64_t i = grp; i < nmine; i += kGroups) {
-    const int b = static_cast<int>(i % kBufs);
+  // 32-bit tile bookkeeping (ntiles < 2^31; nblk = C / CW is a power of two)
+  const int lg_nblk = __ffs(static_cast<int>(nblk)) - 1;
+  const int nm = static_cast<int>(nmine), st32 = static_cast<int>(step);
+  for (int i = grp; i < nm; i += kGroups) {
+    const int b = i % kBufs;
     T2* const buf = bufs + b * kFftElems;
-    const int64_t t = blockIdx.x + i * step;
+    const int t = static_cast<int>(blockIdx.x) + i * st32;
+    const int blk = t & ((1 << lg_nblk) - 1), ck = t >> lg_nblk;
     // fp32: the base/step twiddles are loaded before the FFT (they land during it); fp64 has
     // no registers to spare across the transform and loads them after it (one L1 latency)
     PassATwiddles<T2> tw2;
     if constexpr (sizeof(Real) == 4) {
       int fl, out0l, stl;
       last_stage_out(gt, lgR, lgCW, fl, out0l, stl);
-      tw2 = pass_a_twiddles((t % nblk) * CW + fl, out0l, stl, mr, lo_bits, tw_hi, tw_lo);
+      tw2 = pass_a_twiddles(static_cast<int64_t>(blk * CW + fl), out0l, stl, mr, lo_bits, tw_hi, tw_lo);
     }
     mbar_wait(&bars[b], static_cast<uint32_t>((i / kBufs) & 1));
     T2 v[16];
@@ -493,25 +497,25 @@ __global__ void __launch_bounds__(kFftThreads * kGroups, 1) fft_cols_async_kerne
     group_bar(1 + grp);  // stage 0 runs in place
     int f, out0, st;
     fft16_regs<R0, false>(v, buf, lgR, lgCW, CW, 1, tw_r, f, out0, st, 1 + grp, gt);
-    const int64_t blk = t % nblk, ck = t / nblk;
-    const int64_t ch = ck / k, kk = ck - ch * k;
-    T2* g = out + (ch * kpad + kk) * mr;  // out of place: the blocked input is still being read
-    const int64_t j2 = blk * CW + f;
-    if constexpr (sizeof(Real) == 8) tw2 = pass_a_twiddles(j2, out0, st, mr, lo_bits, tw_hi, tw_lo);
+    const int ch = ck / k, kk = ck - ch * k;
+    T2* g = out + (static_cast<int64_t>(ch) * kpad + kk) * mr;  // out of place: the blocked input is still being read
+    const int j2 = blk * CW + f;
+    if constexpr (sizeof(Real) == 8) tw2 = pass_a_twiddles(static_cast<int64_t>(j2), out0, st, mr, lo_bits, tw_hi, tw_lo);
     // inter-pass twiddles w_Mr^{j2 k1}, k1 = out0 + q st: w_base * w_step^q (base and step were
     // loaded from the two-level table before the FFT; 15 complex products instead of 30 loads)
     T2 w = cmul(tw2.b_hi, tw2.b_lo);
     const T2 wstep = cmul(tw2.s_hi, tw2.s_lo);
+    T2* gr = g + j2 + static_cast<int64_t>(out0) * C;
+    const int64_t rstep = static_cast<int64_t>(st) * C;
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
-      const int k1 = out0 + q * st;
-      g[static_cast<int64_t>(k1) * C + j2] = cmul(v[q], w);  // natural row-major layout for pass B
+      gr[q * rstep] = cmul(v[q], w);  // natural row-major layout for pass B
       if (q < 15) w = cmul(w, wstep);
     }
     group_bar(1 + grp);  // buf consumed: refill it with tile i + 3
-    if (gt == 0 && i + kBufs < nmine)
-      issue_cols_tile(buf, cols_tile_src(grid, blockIdx.x + (i + kBufs) * step, nblk, k, kpad, mr), zeros, R, CW,
-                      row_lo, row_cnt, &bars[b]);
+    if (gt == 0 && i + kBufs < nm)
+      issue_cols_tile(buf, cols_tile_src(grid, blockIdx.x + static_cast<int64_t>(i + kBufs) * step, nblk, k, kpad, mr),
+                      zeros, R, CW, row_lo, row_cnt, &bars[b]);
   }
 }
 
