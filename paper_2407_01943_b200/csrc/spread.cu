@@ -223,46 +223,59 @@ __device__ inline void dmma_8x8x4(double& d0, double& d1, double a, double b) {
                : "d"(a), "d"(b));
 }
 
-// A warp's walk over its rounds: item = channel * nseg + segment; each segment visits its
-// wrapping points (part 0, segments with s0 < w2-1) then its own (part 1), 32 at a time; a
-// segment without points still yields one empty round so that its cells are written.  Only
-// the furthest cursor advances; the segment range it will need next is prefetched one item
-// ahead (`pre`), so no cursor step waits on a global load.
+// A warp's walk over its rounds: item = channel * nseg_used + s (s indexes the channel's used
+// segments); each segment visits its wrapping points (part 0, segments with s0 < w2-1) then
+// its own (part 1), 32 at a time; a segment without points still yields one empty round so
+// that its cells are written.  Only the furthest cursor advances; the segment range it will
+// need next is prefetched one item ahead (`pre`, at position `pp`), so no cursor step waits on
+// a global load.  Items are carried as (channel, s) and stepped by the stride with a wrap, so
+// the walk has no integer division.
 struct TcCursor {
-  int64_t item, c, seg, shift;
-  int part, b0, hi, nb, own_lo, own_hi;
+  int64_t seg, shift;
+  int c, part, b0, hi, nb, own_lo, own_hi;
   bool valid, last;
 };
+struct TcPos {
+  int c, s;
+};
 
-// item -> (channel, segment): the channel's segments of rows row_lo .. row_lo + row_cnt - 1
 template <typename Real>
-__device__ inline void tc_item(int64_t item, const SpreadParams<Real>& P, int64_t& c, int64_t& seg) {
-  c = item / P.nseg_used;
-  const int64_t s = item - c * P.nseg_used;
+__device__ inline void tc_step(TcPos& p, int stride, const SpreadParams<Real>& P) {
+  p.s += stride;
+  while (p.s >= static_cast<int>(P.nseg_used)) {
+    p.s -= static_cast<int>(P.nseg_used);
+    ++p.c;
+  }
+}
+
+// used-segment index -> segment: rows row_lo .. row_lo + row_cnt - 1 (cyclic) of the channel
+template <typename Real>
+__device__ inline int64_t tc_seg(int s, const SpreadParams<Real>& P) {
   const int64_t row = ((s >> P.lg_spr) + P.row_lo) & (P.nrows - 1);
-  seg = (row << P.lg_spr) | (s & ((int64_t{1} << P.lg_spr) - 1));
+  return (row << P.lg_spr) | (s & ((1 << P.lg_spr) - 1));
 }
 
 template <typename Real>
-__device__ inline int4 tc_range(int64_t item, int64_t total, const SpreadParams<Real>& P) {
+__device__ inline int4 tc_range(TcPos p, const SpreadParams<Real>& P) {
   // unconditional (clamped) load: a conditional one merges with a default and the merge
   // waits on the load; past-the-end items are never settled (valid = false)
-  int64_t c, seg;
-  tc_item(min(item, total - 1), P, c, seg);
-  return reinterpret_cast<const int4*>(P.seg_ranges)[c * P.nseg + seg];
+  const bool ok = p.c < static_cast<int>(P.channels);
+  const int c = ok ? p.c : static_cast<int>(P.channels) - 1;
+  const int s = ok ? p.s : static_cast<int>(P.nseg_used) - 1;
+  return reinterpret_cast<const int4*>(P.seg_ranges)[static_cast<int64_t>(c) * P.nseg + tc_seg(s, P)];
 }
 
 template <typename Real>
-__device__ inline void tc_settle(TcCursor& u, int64_t item, int4 r, const SpreadParams<Real>& P, int64_t total) {
-  u.item = item;
-  if (item >= total) {
+__device__ inline void tc_settle(TcCursor& u, TcPos p, int4 r, const SpreadParams<Real>& P) {
+  if (p.c >= static_cast<int>(P.channels)) {
     u.valid = false;
     u.nb = 0;
     u.last = false;
     return;
   }
   u.valid = true;
-  tc_item(item, P, u.c, u.seg);
+  u.c = p.c;
+  u.seg = tc_seg(p.s, P);
   u.own_lo = r.x;
   u.own_hi = r.y;
   if (r.z < static_cast<int>(P.n)) {
@@ -281,8 +294,7 @@ __device__ inline void tc_settle(TcCursor& u, int64_t item, int4 r, const Spread
 }
 
 template <typename Real>
-__device__ inline void tc_advance(TcCursor& u, int4& pre, const SpreadParams<Real>& P, int64_t total,
-                                  int64_t stride) {
+__device__ inline void tc_advance(TcCursor& u, int4& pre, TcPos& pp, const SpreadParams<Real>& P, int stride) {
   if (!u.valid) return;
   if (u.b0 + 32 < u.hi) {
     u.b0 += 32;
@@ -292,10 +304,11 @@ __device__ inline void tc_advance(TcCursor& u, int4& pre, const SpreadParams<Rea
     u.hi = u.own_hi;
     u.shift = u.seg * 32;
   } else {
-    const int64_t next = u.item + stride;
-    const int4 r = pre;  // = range(next), loaded one item ago
-    pre = tc_range(next + stride, total, P);
-    tc_settle(u, next, r, P, total);
+    const TcPos next = pp;  // its range is `pre`, loaded one item ago
+    const int4 r = pre;
+    tc_step(pp, stride, P);
+    pre = tc_range(pp, P);
+    tc_settle(u, next, r, P);
     return;
   }
   u.nb = min(32, u.hi - u.b0);
@@ -321,7 +334,7 @@ __device__ inline void tc_load(TcPoint<Real>& q, int ti, const TcCursor& u, int 
   if (!u.valid || u.nb == 0) return;  // warp-uniform
   const bool has = lane < u.nb;
   const int j = has ? lane : u.nb - 1;
-  const int64_t base = u.c * P.n;
+  const int64_t base = static_cast<int64_t>(u.c) * P.n;
   const int64_t gi = base + u.b0 + j;
   q.ti = has ? ti : -1;
   const int64_t xi = base + (has ? ti : 0);
@@ -337,14 +350,15 @@ __device__ inline void tc_load(TcPoint<Real>& q, int ti, const TcCursor& u, int 
   }
   q.ph = reinterpret_cast<const R2*>(P.prephase)[gi];
   q.ag = P.gauss[gi];
-  const Real* tp = P.taper_base + (u.c * P.k_total + P.k0) * P.tstride_k + (u.b0 + j) * P.tstride_j;
+  const Real* tp =
+      P.taper_base + (static_cast<int64_t>(u.c) * P.k_total + P.k0) * P.tstride_k + (u.b0 + j) * P.tstride_j;
 #pragma unroll
   for (int k = 0; k < 8; ++k) q.w[k] = tp[min(k, P.kg - 1) * P.tstride_k];
 }
 
 template <typename Real>
 __device__ inline int tc_perm(const TcCursor& u, int lane, const SpreadParams<Real>& P) {
-  return (u.valid && lane < u.nb) ? P.perm[u.c * P.n + u.b0 + lane] : 0;
+  return (u.valid && lane < u.nb) ? P.perm[static_cast<int64_t>(u.c) * P.n + u.b0 + lane] : 0;
 }
 
 template <typename Real, int XK>
@@ -366,16 +380,18 @@ __global__ void __launch_bounds__(kTcWarps * 32, kTcCtasPerSm) spread_tc_kernel(
   for (int i = lane; i < RS; i += 32) srel[i] = 1 << 20;  // absent points: outside every block
   __syncthreads();
 
-  const int64_t total = P.nseg_used * P.channels;
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * kTcWarps;
-  const int64_t item0 = static_cast<int64_t>(blockIdx.x) * kTcWarps + warp;
+  const int stride = static_cast<int>(gridDim.x) * kTcWarps;
+  TcPos p0{0, static_cast<int>(blockIdx.x) * kTcWarps + warp};
+  tc_step(p0, 0, P);  // normalise (fewer used segments than warps)
+  TcPos pp = p0;
+  tc_step(pp, stride, P);
   TcCursor cur, n1, n2;
-  int4 pre = tc_range(item0 + stride, total, P);
-  tc_settle(cur, item0, tc_range(item0, total, P), P, total);
+  int4 pre = tc_range(pp, P);
+  tc_settle(cur, p0, tc_range(p0, P), P);
   n1 = cur;
-  tc_advance(n1, pre, P, total, stride);
+  tc_advance(n1, pre, pp, P, stride);
   n2 = n1;
-  tc_advance(n2, pre, P, total, stride);
+  tc_advance(n2, pre, pp, P, stride);
   TcPoint<Real> pt;
   pt.ti = -1;
   tc_load<Real, XK>(pt, tc_perm(cur, lane, P), cur, lane, P);
@@ -451,7 +467,7 @@ __global__ void __launch_bounds__(kTcWarps * 32, kTcCtasPerSm) spread_tc_kernel(
       }
     }
     if (cur.last) {
-      R2* out = P.grid + (cur.c * P.kpad + P.k0) * P.mr;
+      R2* out = P.grid + (static_cast<int64_t>(cur.c) * P.kpad + P.k0) * P.mr;
       R2* out0 = out + off_h0;
       R2* out1 = out + off_h1;
       const bool k0ok = 2 * t < P.kg, k1ok = 2 * t + 1 < P.kg;
@@ -467,7 +483,7 @@ __global__ void __launch_bounds__(kTcWarps * 32, kTcCtasPerSm) spread_tc_kernel(
     __syncwarp();  // private tables are restaged next
     cur = n1;
     n1 = n2;
-    tc_advance(n2, pre, P, total, stride);
+    tc_advance(n2, pre, pp, P, stride);
   }
 }
 
