@@ -561,19 +561,22 @@ __global__ void __launch_bounds__(kFftThreads * kGroups, 1) fft_rows_crop_async_
     for (int b = 0; b < kBufs && b < nunits; ++b) issue(b, b);
   }
   __syncthreads();
-  Real acc[16];
+  Real acc[kCropN];
 #pragma unroll
-  for (int q = 0; q < 16; ++q) acc[q] = Real(0);
-  for (int64_t i = grp; i < nunits; i += kGroups) {
-    const int b = static_cast<int>(i % kBufs);
+  for (int c = 0; c < kCropN; ++c) acc[c] = Real(0);
+  const int nu = static_cast<int>(nunits);
+  for (int i = grp; i < nu; i += kGroups) {
+    const int b = i % kBufs;
     T2* const buf = bufs + b * kFftElems;
-    int64_t row, kk;
-    const bool live = rows_unit(i, k_count, nrows, row, kk);  // uniform over the group
+    // unit i = 2 m + g: group g's m-th unit, row rl = 2 (m / K) + g of this CTA, taper m % K
+    const int m = i >> 1, mq = m / k_count, kk = m - mq * k_count;
+    const int row = static_cast<int>(blockIdx.x) + (kGroups * mq + grp) * static_cast<int>(gridDim.x);
+    const bool live = row < static_cast<int>(nrows);  // uniform over the group
     // every unit waits for its phase, live or not: a group must never run ahead and refill a
     // buffer (unit i + 3) before that buffer's current unit has been issued and consumed
     mbar_wait(&bars[b], static_cast<uint32_t>((i / kBufs) & 1));
     if (live) {
-      const int64_t ch = row / R, k1 = row - ch * R;
+      const int ch = row / R, k1 = row - ch * R;
       T2 v[16];
 #pragma unroll
       for (int sl = 0; sl < 16; ++sl) {
@@ -585,9 +588,10 @@ __global__ void __launch_bounds__(kFftThreads * kGroups, 1) fft_rows_crop_async_
       int f = 0, out0 = 0, st = 1;
       fft16_regs<R0, true>(v, buf, lgC, 0, 1, C, tw_c, f, out0, st, 1 + grp, gt);
 #pragma unroll
-      for (int q = 0; q < 16; ++q) {
+      for (int c = 0; c < kCropN; ++c) {
+        const int q = crop_q(c);
         const T2 x = v[q];
-        acc[q] += x.x * x.x + x.y * x.y;
+        acc[c] += x.x * x.x + x.y * x.y;
         if (j_out) {
           const int64_t kb = k1 + static_cast<int64_t>(R) * (out0 + q * st);
           int64_t ii = -1;
@@ -595,32 +599,40 @@ __global__ void __launch_bounds__(kFftThreads * kGroups, 1) fft_rows_crop_async_
           else if (mr - kb < nc - mode_offset) ii = mode_offset + (mr - kb);
           if (ii >= 0 && ii < nc) {
             const Real d = deconv[ii];
-            j_out[(ch * k_count + kk) * nc + ii] = T2{d * x.x, d * x.y};
+            j_out[(static_cast<int64_t>(ch) * k_count + kk) * nc + ii] = T2{d * x.x, d * x.y};
           }
         }
       }
       if (kk == k_count - 1) {
         if (power) {
+          int64_t iv[kCropN];
+          Real dv[kCropN];
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const int64_t kb = k1 + static_cast<int64_t>(R) * (out0 + q * st);
+          for (int c = 0; c < kCropN; ++c) {  // all nine loads in flight before the first use
+            const int64_t kb = k1 + static_cast<int64_t>(R) * (out0 + crop_q(c) * st);
             int64_t ii = -1;
             if (kb <= mode_offset) ii = mode_offset - kb;
             else if (mr - kb < nc - mode_offset) ii = mode_offset + (mr - kb);
+            iv[c] = ii;
+            dv[c] = deconv[ii < 0 ? 0 : (ii < nc ? ii : nc - 1)];
+          }
+#pragma unroll
+          for (int c = 0; c < kCropN; ++c) {
+            const int64_t ii = iv[c];
             if (ii >= 0 && ii < nc) {
-              const double d = static_cast<double>(deconv[ii]);
-              const PReal val = static_cast<PReal>(d * d * static_cast<double>(acc[q]) / divisor);
-              PReal* dst = power + ch * nc + ii;
+              const double d = static_cast<double>(dv[c]);
+              const PReal val = static_cast<PReal>(d * d * static_cast<double>(acc[c]) / divisor);
+              PReal* dst = power + static_cast<int64_t>(ch) * nc + ii;
               *dst = accumulate ? *dst + val : val;
             }
           }
         }
 #pragma unroll
-        for (int q = 0; q < 16; ++q) acc[q] = Real(0);
+        for (int c = 0; c < kCropN; ++c) acc[c] = Real(0);
       }
     }
     group_bar(1 + grp);  // buf consumed: refill it with unit i + 3
-    if (gt == 0 && i + kBufs < nunits) issue(i + kBufs, b);
+    if (gt == 0 && i + kBufs < nu) issue(i + kBufs, b);
   }
 }
 
@@ -792,7 +804,7 @@ void launch_rows(const Plan& plan, void* grid, int64_t k, int64_t kpad, void* j_
   auto* g = static_cast<const T2*>(grid);
   const int r0 = first_radix(f.C);
   // The bulk-copy pass B is correct but measured slower than the register-loading kernel
-  // on C2 (0.114 vs 0.105 ms): opt in with NUS_FFT_ASYNC_B=1.
+  // on C2 (0.102 vs 0.097 ms): opt in with NUS_FFT_ASYNC_B=1.
   static const bool async_b = fused_pass_b_async();
   if (use_async(f, sizeof(T2)) && r0 == 16 && async_b) {
     const int64_t nrows = p.channels * f.R;
