@@ -129,11 +129,12 @@ __device__ inline int sidx(int e) {
 // u = tid + bb*256; on exit v[q] = output element (f_out, out0 + q*Ns_last).
 // Barrier over the kFftThreads threads that share one in-CTA FFT: id 0 with a 256-thread CTA
 // is __syncthreads(); the grouped kernels run two such groups per CTA on ids 1 and 2.
+template <int NT = kFftThreads>
 __device__ inline void group_bar(int id) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(kFftThreads) : "memory");
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(NT) : "memory");
 }
 
-template <int R0, bool SWZ, typename T2>
+template <int R0, bool SWZ, typename T2, int NT = kFftThreads>
 __device__ inline void fft16_regs(T2 (&v)[16], T2* buf, int lgL, int lgNfft, int es, int fs,
                                   const T2* __restrict__ tw, int& f_out, int& out0, int& step_out, int bar = 0,
                                   int tid = -1) {
@@ -150,14 +151,14 @@ __device__ inline void fft16_regs(T2 (&v)[16], T2* buf, int lgL, int lgNfft, int
     for (int bb = 0; bb < B0; ++bb) {
       T2* g = v + bb * R0;
       dft_reg<R0>(g);
-      const int u = tid + bb * kFftThreads;
+      const int u = tid + bb * NT;
       const int f = u & nfm, j = (u >> lgNfft) & ((1 << lgNb) - 1);
       const int base = f * fs + (j << lgR0) * es;  // Ns = 1: out = j*R0 + q
 #pragma unroll
       for (int q = 0; q < R0; ++q) buf[sidx<SWZ>(base + q * es)] = g[q];
     }
   }
-  group_bar(bar);
+  group_bar<NT>(bar);
   // ---- radix-16 stages; the last keeps its outputs in registers
   const int lgNb = lgL - 4;
   const int u = tid;
@@ -182,10 +183,10 @@ __device__ inline void fft16_regs(T2 (&v)[16], T2* buf, int lgL, int lgNfft, int
     dft_reg<16>(v);
     const int outb = f * fs + (((j - jm) << 4) + jm) * es;
     if (lgNs + 4 < lgL) {
-      group_bar(bar);
+      group_bar<NT>(bar);
 #pragma unroll
       for (int q = 0; q < 16; ++q) buf[sidx<SWZ>(outb + (q << lgNs) * es)] = v[q];
-      group_bar(bar);
+      group_bar<NT>(bar);
     } else {
       f_out = f;
       out0 = ((j - jm) << 4) + jm;
@@ -195,13 +196,13 @@ __device__ inline void fft16_regs(T2 (&v)[16], T2* buf, int lgL, int lgNfft, int
 }
 
 // Stage-0 input index of register slot (bb, q) for this thread: element j + q*L/R0 of FFT f.
-template <int R0>
+template <int R0, int NT = kFftThreads>
 __device__ inline void stage0_index(int slot, int lgL, int lgNfft, int& f, int& e, int tid = -1) {
   if (tid < 0) tid = threadIdx.x;
   constexpr int lgR0 = R0 == 16 ? 4 : R0 == 8 ? 3 : R0 == 4 ? 2 : 1;
   const int bb = slot / R0, q = slot % R0;
   const int lgNb = lgL - lgR0;
-  const int u = tid + bb * kFftThreads;
+  const int u = tid + bb * NT;
   f = u & ((1 << lgNfft) - 1);
   const int j = (u >> lgNfft) & ((1 << lgNb) - 1);
   e = j + (q << lgNb);
@@ -275,8 +276,10 @@ __global__ void __launch_bounds__(kFftThreads, 2) fft_cols_kernel(
 constexpr int kCropN = 9;  // last-stage outputs q the crop can keep (pass B, Mr >= 2 nc)
 __host__ __device__ constexpr int crop_q(int c) { return c < 5 ? c : c + 7; }
 
-template <typename Real, typename PReal, int R0>
-__global__ void __launch_bounds__(kFftThreads, 2) fft_rows_crop_kernel(
+// NT threads per row: 256 for C = 4096 (2 CTAs / SM), 128 for C = 2048 (4 CTAs / SM, twice the
+// rows in flight to cover the row loads).
+template <typename Real, typename PReal, int R0, int NT = kFftThreads>
+__global__ void __launch_bounds__(NT, NT == 128 ? 4 : 2) fft_rows_crop_kernel(
     const typename C2<Real>::T* __restrict__ grid, int64_t mr, int R, int C, int RPC, int64_t kpad,
     int k_count, int64_t nc, int64_t mode_offset, const Real* __restrict__ deconv,
     const typename C2<Real>::T* __restrict__ tw_c, typename C2<Real>::T* __restrict__ j_out,
@@ -299,10 +302,10 @@ __global__ void __launch_bounds__(kFftThreads, 2) fft_rows_crop_kernel(
 #pragma unroll
     for (int s = 0; s < 16; ++s) {
       int ff, e;
-      stage0_index<R0>(s, lgC, 0, ff, e);
+      stage0_index<R0, NT>(s, lgC, 0, ff, e);
       v[s] = g[e];
     }
-    fft16_regs<R0, true>(v, buf, lgC, 0, 1, C, tw_c, f, out0, step);
+    fft16_regs<R0, true, T2, NT>(v, buf, lgC, 0, 1, C, tw_c, f, out0, step);
 #pragma unroll
     for (int c = 0; c < kCropN; ++c) {
       const int q = crop_q(c);
@@ -669,7 +672,13 @@ void fused_fft_prepare(Plan& plan) {
   // 256 threads x 16 registers: every in-CTA FFT holds exactly 4096 elements.
   // Rows: C = 4096 (pass B, one row per CTA); columns: R = Mr / 4096 with CW = 4096 / R
   // consecutive columns per CTA (>= 128-byte row segments for R <= 512).
-  f.C = kFftElems;
+  // 2048-point rows (pass B at 4 CTAs / SM) whenever the pass-A tile still holds whole
+  // columns (R = Mr / 2048 <= 4096); NUS_FFT_C=4096 keeps 4096-point rows
+  {
+    const char* e = std::getenv("NUS_FFT_C");
+    const bool c4096 = e && std::strcmp(e, "4096") == 0;
+    f.C = (!c4096 && p.mr >= (int64_t{1} << 17) && p.mr <= (int64_t{1} << 23)) ? kFftElems / 2 : kFftElems;
+  }
   f.R = static_cast<int>(p.mr / f.C);
   f.RPC = 1;
   f.CW = f.R > 1 ? kFftElems / f.R : 0;
@@ -806,7 +815,7 @@ void launch_rows(const Plan& plan, void* grid, int64_t k, int64_t kpad, void* j_
   // The bulk-copy pass B is correct but measured slower than the register-loading kernel
   // on C2 (0.102 vs 0.097 ms): opt in with NUS_FFT_ASYNC_B=1.
   static const bool async_b = fused_pass_b_async();
-  if (use_async(f, sizeof(T2)) && r0 == 16 && async_b) {
+  if (use_async(f, sizeof(T2)) && r0 == 16 && f.C == kFftElems && async_b) {
     const int64_t nrows = p.channels * f.R;
     const unsigned grid_x = static_cast<unsigned>(std::min<int64_t>(nrows, sm_count()));
     const size_t smem_a = kBufs * static_cast<size_t>(kFftElems) * sizeof(T2) + kBufs * sizeof(uint64_t);
@@ -815,14 +824,16 @@ void launch_rows(const Plan& plan, void* grid, int64_t k, int64_t kpad, void* j_
         f.tw_c.as<T2>(), static_cast<T2*>(j_out), static_cast<PReal*>(power), divisor, acc);
     return;
   }
-#define NUS_ROWS(R0)                                                                                    \
-  fft_rows_crop_kernel<Real, PReal, R0><<<gb, kFftThreads, smem, s>>>(                                  \
+#define NUS_ROWS(R0, NT)                                                                                \
+  fft_rows_crop_kernel<Real, PReal, R0, NT><<<gb, NT, smem, s>>>(                                       \
       g, p.mr, f.R, f.C, 1, kpad, static_cast<int>(k), p.nc, p.mode_offset, plan.tab.deconv.as<Real>(), \
       f.tw_c.as<T2>(), static_cast<T2*>(j_out), static_cast<PReal*>(power), divisor, acc)
-  if (r0 == 16) NUS_ROWS(16);
-  else if (r0 == 8) NUS_ROWS(8);
-  else if (r0 == 4) NUS_ROWS(4);
-  else NUS_ROWS(2);
+  if (f.C == kFftElems / 2) {  // 2048-point rows, 128 threads
+    NUS_ROWS(8, 128);
+  } else if (r0 == 16) NUS_ROWS(16, kFftThreads);
+  else if (r0 == 8) NUS_ROWS(8, kFftThreads);
+  else if (r0 == 4) NUS_ROWS(4, kFftThreads);
+  else NUS_ROWS(2, kFftThreads);
 #undef NUS_ROWS
 }
 
