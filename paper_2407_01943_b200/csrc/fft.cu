@@ -271,6 +271,47 @@ __global__ void __launch_bounds__(kFftThreads, 2) fft_cols_kernel(
   }
 }
 
+// Pass A over the blocked grid with register loads: one tile (R rows x CW columns, contiguous,
+// NT * 16 elements) per CTA, several CTAs per SM in flight instead of a persistent bulk-copy
+// pipeline.  Rows outside the occupied interval are zeros and are not read.
+template <typename Real, int R0, int NT>
+__global__ void __launch_bounds__(NT, NT == 128 ? 4 : 2) fft_cols_blk_kernel(
+    const typename C2<Real>::T* __restrict__ grid, typename C2<Real>::T* __restrict__ out, int64_t mr, int R, int C,
+    int CW, int k, int kpad, const typename C2<Real>::T* __restrict__ tw_r,
+    const typename C2<Real>::T* __restrict__ tw_hi, const typename C2<Real>::T* __restrict__ tw_lo, int lo_bits,
+    int row_lo, int row_cnt) {
+  using T2 = typename C2<Real>::T;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T2* const buf = reinterpret_cast<T2*>(smem_raw);  // [R][CW]
+  const int lgR = __ffs(R) - 1, lgCW = __ffs(CW) - 1, lg_nblk = __ffs(C / CW) - 1;
+  const int t = blockIdx.x;
+  const int blk = t & ((1 << lg_nblk) - 1), ck = t >> lg_nblk;
+  const int ch = ck / k, kk = ck - ch * k;
+  const T2* src = grid + (static_cast<int64_t>(ch) * kpad + kk) * mr + (static_cast<int64_t>(blk) << (lgR + lgCW));
+  T2 v[16];
+#pragma unroll
+  for (int sl = 0; sl < 16; ++sl) {
+    int f, e;
+    stage0_index<R0, NT>(sl, lgR, lgCW, f, e);
+    const bool occ = static_cast<unsigned>((e - row_lo) & (R - 1)) < static_cast<unsigned>(row_cnt);
+    v[sl] = occ ? src[e * CW + f] : T2{Real(0), Real(0)};
+  }
+  int f, out0, st;
+  fft16_regs<R0, false, T2, NT>(v, buf, lgR, lgCW, CW, 1, tw_r, f, out0, st);
+  T2* g = out + (static_cast<int64_t>(ch) * kpad + kk) * mr;
+  const int j2 = blk * CW + f;
+  const PassATwiddles<T2> tw2 = pass_a_twiddles(static_cast<int64_t>(j2), out0, st, mr, lo_bits, tw_hi, tw_lo);
+  T2 w = cmul(tw2.b_hi, tw2.b_lo);
+  const T2 wstep = cmul(tw2.s_hi, tw2.s_lo);
+  T2* gr = g + j2 + static_cast<int64_t>(out0) * C;
+  const int64_t rstep = static_cast<int64_t>(st) * C;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    gr[q * rstep] = cmul(v[q], w);
+    if (q < 15) w = cmul(w, wstep);
+  }
+}
+
 // ---- pass B + crop / power ---------------------------------------------------------------
 
 constexpr int kCropN = 9;  // last-stage outputs q the crop can keep (pass B, Mr >= 2 nc)
@@ -446,7 +487,7 @@ template <typename T2>
 __device__ inline const T2* cols_tile_src(const T2* grid, int64_t t, int64_t nblk, int k, int kpad, int64_t mr) {
   const int64_t blk = t % nblk, ck = t / nblk;
   const int64_t ch = ck / k, kk = ck - ch * k;
-  return grid + (ch * kpad + kk) * mr + blk * kFftElems;
+  return grid + (ch * kpad + kk) * mr + blk * kFftElems;  // bulk-copy pass A: tiles of 4096 (cols_mode 2)
 }
 
 template <typename Real, int R0>
@@ -681,7 +722,14 @@ void fused_fft_prepare(Plan& plan) {
   }
   f.R = static_cast<int>(p.mr / f.C);
   f.RPC = 1;
-  f.CW = f.R > 1 ? kFftElems / f.R : 0;
+  {  // pass A: register-loading 4096-cell tiles (default; 96.4 vs 107.4 us for the bulk-copy
+     // pipeline and 114 us for 2048-cell tiles, whose 32-byte row segments coalesce poorly)
+    const char* e = std::getenv("NUS_FFT_COLS");
+    f.cols_mode = (e && std::strcmp(e, "async") == 0) ? 2 : (e && std::strcmp(e, "reg128") == 0) ? 0 : 1;
+  }
+  if (f.cols_mode == 0 && f.R > kFftElems / 2) f.cols_mode = 1;  // a 2048-cell tile must hold >= 1 column
+  const int tile = f.cols_mode == 0 ? kFftElems / 2 : kFftElems;
+  f.CW = f.R > 1 ? tile / f.R : 0;
   f.lo_bits = lg / 2;
   // blocked grid layout + bulk-copy (asynchronous) passes unless NUS_FFT_ASYNC=0
   {
@@ -689,6 +737,7 @@ void fused_fft_prepare(Plan& plan) {
     f.blocked = f.R > 1 && !(e && std::strcmp(e, "0") == 0);
     f.lgC = ilog2(f.C);
     f.lgCW = f.CW > 0 ? ilog2(f.CW) : 0;
+    f.lgT = ilog2(f.R) + f.lgCW;
   }
   const bool f64 = p.precision == NUS_F64;
   const size_t cb = f64 ? sizeof(double2) : sizeof(float2);
@@ -722,6 +771,10 @@ void fused_fft_prepare(Plan& plan) {
     NUS_ATTR((fft_cols_kernel<double, 4>));
     NUS_ATTR((fft_cols_kernel<double, 2>));
     NUS_ATTR((fft_rows_crop_kernel<double, double, 16>));
+    NUS_ATTR((fft_cols_blk_kernel<double, 16, kFftThreads>));
+    NUS_ATTR((fft_cols_blk_kernel<double, 8, kFftThreads>));
+    NUS_ATTR((fft_cols_blk_kernel<double, 4, kFftThreads>));
+    NUS_ATTR((fft_cols_blk_kernel<double, 2, kFftThreads>));
 #undef NUS_ATTR
     const int smem2 = kBufs * kFftElems * static_cast<int>(sizeof(double2)) + kBufs * 8;
 #define NUS_ATTR2(KERN) NUS_CUDA(cudaFuncSetAttribute(KERN, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2))
@@ -773,6 +826,27 @@ void launch_cols(const Plan& plan, void* grid, void* scratch, int64_t k, int64_t
   auto* g = static_cast<T2*>(grid);
   const T2 *tr = f.tw_r.as<T2>(), *th = f.tw_hi.as<T2>(), *tl = f.tw_lo.as<T2>();
   const int r0 = first_radix(f.R);
+  if (use_async(f, sizeof(T2)) && f.cols_mode != 2) {
+    const int64_t ntiles = p.channels * k * (f.C / f.CW);
+    auto* out = static_cast<T2*>(scratch);
+#define NUS_COLS_REG(R0, NT)                                                                                 \
+  fft_cols_blk_kernel<Real, R0, NT><<<static_cast<unsigned>(ntiles), NT, static_cast<size_t>(NT) * 16 * sizeof(T2), \
+                                      s>>>(g, out, p.mr, f.R, f.C, f.CW, static_cast<int>(k), static_cast<int>(kpad), \
+                                           tr, th, tl, f.lo_bits, f.row_lo, f.row_cnt)
+    if (f.cols_mode == 0) {
+      if (r0 == 16) NUS_COLS_REG(16, 128);
+      else if (r0 == 8) NUS_COLS_REG(8, 128);
+      else if (r0 == 4) NUS_COLS_REG(4, 128);
+      else NUS_COLS_REG(2, 128);
+    } else {
+      if (r0 == 16) NUS_COLS_REG(16, kFftThreads);
+      else if (r0 == 8) NUS_COLS_REG(8, kFftThreads);
+      else if (r0 == 4) NUS_COLS_REG(4, kFftThreads);
+      else NUS_COLS_REG(2, kFftThreads);
+    }
+#undef NUS_COLS_REG
+    return;
+  }
   if (use_async(f, sizeof(T2))) {
     const int64_t ntiles = p.channels * k * (f.C / f.CW);
     T2* out = static_cast<T2*>(scratch);
@@ -850,7 +924,10 @@ void fft_stage_names(const Plan& plan, const char** a, const char** b) {
     *b = "crop_power_kernel";
     return;
   }
-  *a = plan.ffft.R <= 1 ? "(none: single pass)" : plan.ffft.blocked ? "fft_cols_async_kernel" : "fft_cols_kernel";
+  *a = plan.ffft.R <= 1          ? "(none: single pass)"
+       : !plan.ffft.blocked        ? "fft_cols_kernel"
+       : plan.ffft.cols_mode == 2  ? "fft_cols_async_kernel"
+                                   : "fft_cols_blk_kernel";
   *b = (plan.ffft.blocked && fused_pass_b_async()) ? "fft_rows_crop_async_kernel" : "fft_rows_crop_kernel";
 }
 

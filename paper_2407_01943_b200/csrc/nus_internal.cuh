@@ -112,9 +112,12 @@ struct FusedFft {
   bool ready = false;
   int R = 1, C = 1, RPC = 1, CW = 0, lo_bits = 0;
   // blocked: the spread writes cell j1*C + j2 at (j2/CW)*R*CW + j1*CW + j2%CW so that every
-  // pass-A column block is contiguous (bulk-copied); lgC/lgCW are its shifts
+  // pass-A column block (tile, 2^lgT = R*CW cells) is contiguous; lgC/lgCW/lgT are its shifts
   bool blocked = false;
-  int lgC = 0, lgCW = 0;
+  int lgC = 0, lgCW = 0, lgT = 12;
+  // pass A over the blocked grid: 1 = register-loading tiles of 4096 (256 threads, default),
+  // 0 = tiles of 2048 (128 threads), 2 = bulk-copy pipeline (NUS_FFT_COLS=reg128 / async)
+  int cols_mode = 1;
   DeviceBuffer scratch;  // pass-A output (natural layout) when blocked: [C][kpad][Mr]
   // Occupied rows (blocked only): every cell any point's support touches lies in rows
   // j1 in [row_lo, row_lo + row_cnt) (cyclic, union over channels).  The spread writes only

@@ -54,7 +54,7 @@ struct SpreadParams {
   int64_t n, mr, ntiles, kpad, k_total;
   int64_t s0, s1;
   int64_t channels, nseg;
-  int blocked, lgC, lgCW;  // blocked grid layout of the fused FFT (FusedFft::blocked)
+  int blocked, lgC, lgCW, lgT;  // blocked grid layout of the fused FFT (FusedFft::blocked)
   int lg_nseg;
   // items = channels * nseg_used segments: rows (of 2^lg_spr segments) row_lo .. row_lo+row_cnt-1
   // (cyclic mod nrows) of each channel; other rows are never written (FusedFft::row_lo)
@@ -70,17 +70,17 @@ struct SpreadParams {
 };
 
 // Grid address of cell j: natural, or the fused FFT's blocked layout (j = j1 C + j2 stored
-// at (j2 / CW) * 4096 + j1 * CW + j2 % CW, so each pass-A column block is contiguous).
-__device__ inline int64_t cell_addr(int64_t j, int blocked, int lgC, int lgCW) {
+// at (j2 / CW) * 2^lgT + j1 * CW + j2 % CW, so each pass-A column block is contiguous).
+__device__ inline int64_t cell_addr(int64_t j, int blocked, int lgC, int lgCW, int lgT) {
   if (!blocked) return j;
   const int64_t j1 = j >> lgC, j2 = j & ((int64_t{1} << lgC) - 1);
-  return ((j2 >> lgCW) << 12) | (j1 << lgCW) | (j2 & ((int64_t{1} << lgCW) - 1));
+  return ((j2 >> lgCW) << lgT) | (j1 << lgCW) | (j2 & ((int64_t{1} << lgCW) - 1));
 }
 
-__device__ inline int cell_addr32(int j, int blocked, int lgC, int lgCW) {
+__device__ inline int cell_addr32(int j, int blocked, int lgC, int lgCW, int lgT) {
   if (!blocked) return j;
   const int j1 = j >> lgC, j2 = j & ((1 << lgC) - 1);
-  return ((j2 >> lgCW) << 12) | (j1 << lgCW) | (j2 & ((1 << lgCW) - 1));
+  return ((j2 >> lgCW) << lgT) | (j1 << lgCW) | (j2 & ((1 << lgCW) - 1));
 }
 
 template <typename Real, int KG>
@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(kThreads, 5) spread_gather_kernel(const Spread
   if (cell >= P.tile) return;
 #pragma unroll
   for (int k = 0; k < KG; ++k)
-    P.grid[(c * P.kpad + P.k0 + k) * P.mr + cell_addr(c0 + cell, P.blocked, P.lgC, P.lgCW)] = acc[k];
+    P.grid[(c * P.kpad + P.k0 + k) * P.mr + cell_addr(c0 + cell, P.blocked, P.lgC, P.lgCW, P.lgT)] = acc[k];
   (void)lane;
 }
 
@@ -474,7 +474,7 @@ __global__ void __launch_bounds__(kTcWarps * 32, kTcCtasPerSm) spread_tc_kernel(
       const int cell0 = static_cast<int>(cur.seg) * 32 + g;
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
-        const int addr = cell_addr32(cell0 + 8 * b, P.blocked, P.lgC, P.lgCW);
+        const int addr = cell_addr32(cell0 + 8 * b, P.blocked, P.lgC, P.lgCW, P.lgT);
         if (k0ok) out0[addr] = R2{static_cast<Real>(cr[b][0]), static_cast<Real>(ci[b][0])};
         if (k1ok) out1[addr] = R2{static_cast<Real>(cr[b][1]), static_cast<Real>(ci[b][1])};
         cr[b][0] = cr[b][1] = ci[b][0] = ci[b][1] = 0.0;
@@ -583,6 +583,7 @@ void spread_typed(const Plan& plan, const SpreadArgs& a, cudaStream_t s) {
   }
   P.lgC = plan.ffft.lgC;
   P.lgCW = plan.ffft.lgCW;
+  P.lgT = plan.ffft.lgT;
   P.wrap_lo = tb.wrap_lo.as<int32_t>();
   P.tapers = static_cast<const Real*>(a.tapers);
   P.x = a.x;
