@@ -254,7 +254,9 @@ def main():
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize(dev)
-    CAPI.check(L.nus_mtnufft_timing(est.h, args.steps))
+    # the timed region carries no per-stage events: events between the kernels would serialise
+    # the programmatic dependent launches (each kernel's CTAs dispatched while its predecessor
+    # drains); the stage breakdown comes from a separate pass below
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
@@ -274,6 +276,12 @@ def main():
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_max = float(ms_t.item())
+    # stage breakdown: CUDA events around each kernel, a separate pass of the same steps
+    stage_steps = max(1, min(args.steps, 20))
+    CAPI.check(L.nus_mtnufft_timing(est.h, stage_steps))
+    for i in range(stage_steps):
+        step(i)
+    torch.cuda.synchronize(dev)
     stage = np.zeros(3)
     runs = CAPI._i64()
     CAPI.check(L.nus_mtnufft_timing_read(est.h, CAPI.dptr(stage), runs))

@@ -288,6 +288,8 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 4 : 2) fft_cols_blk_kernel(
   const int blk = t & ((1 << lg_nblk) - 1), ck = t >> lg_nblk;
   const int ch = ck / k, kk = ck - ch * k;
   const T2* src = grid + (static_cast<int64_t>(ch) * kpad + kk) * mr + (static_cast<int64_t>(blk) << (lgR + lgCW));
+  pdl_launch_dependents();
+  pdl_wait();  // the spread's grid
   T2 v[16];
 #pragma unroll
   for (int sl = 0; sl < 16; ++sl) {
@@ -337,6 +339,8 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 4 : 2) fft_rows_crop_kernel(
 #pragma unroll
   for (int c = 0; c < kCropN; ++c) acc[c] = Real(0);
   int f = 0, out0 = 0, step = 1;
+  pdl_launch_dependents();
+  pdl_wait();  // pass A's output (and, for power, the previous reader of P)
   for (int kk = 0; kk < k_count; ++kk) {
     const T2* g = grid + (ch * kpad + kk) * mr + static_cast<int64_t>(k1) * C;
     T2 v[16];
@@ -700,6 +704,14 @@ int ilog2(int64_t v) {
 
 }  // namespace
 
+bool pdl_enabled() {  // opt-in: measured slower on C2 (0.312 vs 0.283 ms per spectrum)
+  static const bool on = [] {
+    const char* e = std::getenv("NUS_PDL");
+    return e && std::strcmp(e, "1") == 0;
+  }();
+  return on;
+}
+
 bool fused_fft_supported(const PlanParams& p) {
   // 4096-element in-CTA FFTs need >= 2 stages per pass: C = 4096 rows, R = Mr / 4096 = 1 or >= 32
   return p.mr == kFftElems || (p.mr >= (int64_t{1} << 17) && p.mr <= (int64_t{1} << 24));
@@ -830,9 +842,9 @@ void launch_cols(const Plan& plan, void* grid, void* scratch, int64_t k, int64_t
     const int64_t ntiles = p.channels * k * (f.C / f.CW);
     auto* out = static_cast<T2*>(scratch);
 #define NUS_COLS_REG(R0, NT)                                                                                 \
-  fft_cols_blk_kernel<Real, R0, NT><<<static_cast<unsigned>(ntiles), NT, static_cast<size_t>(NT) * 16 * sizeof(T2), \
-                                      s>>>(g, out, p.mr, f.R, f.C, f.CW, static_cast<int>(k), static_cast<int>(kpad), \
-                                           tr, th, tl, f.lo_bits, f.row_lo, f.row_cnt)
+  launch_pdl(fft_cols_blk_kernel<Real, R0, NT>, dim3(static_cast<unsigned>(ntiles)), dim3(NT),                \
+             static_cast<size_t>(NT) * 16 * sizeof(T2), s, static_cast<const T2*>(g), out, p.mr, f.R, f.C, f.CW, \
+             static_cast<int>(k), static_cast<int>(kpad), tr, th, tl, f.lo_bits, f.row_lo, f.row_cnt)
     if (f.cols_mode == 0) {
       if (r0 == 16) NUS_COLS_REG(16, 128);
       else if (r0 == 8) NUS_COLS_REG(8, 128);
@@ -898,10 +910,10 @@ void launch_rows(const Plan& plan, void* grid, int64_t k, int64_t kpad, void* j_
         f.tw_c.as<T2>(), static_cast<T2*>(j_out), static_cast<PReal*>(power), divisor, acc);
     return;
   }
-#define NUS_ROWS(R0, NT)                                                                                \
-  fft_rows_crop_kernel<Real, PReal, R0, NT><<<gb, NT, smem, s>>>(                                       \
-      g, p.mr, f.R, f.C, 1, kpad, static_cast<int>(k), p.nc, p.mode_offset, plan.tab.deconv.as<Real>(), \
-      f.tw_c.as<T2>(), static_cast<T2*>(j_out), static_cast<PReal*>(power), divisor, acc)
+#define NUS_ROWS(R0, NT)                                                                                  \
+  launch_pdl(fft_rows_crop_kernel<Real, PReal, R0, NT>, gb, dim3(NT), smem, s, g, p.mr, f.R, f.C, 1, kpad, \
+             static_cast<int>(k), p.nc, p.mode_offset, plan.tab.deconv.as<Real>(), f.tw_c.as<T2>(),       \
+             static_cast<T2*>(j_out), static_cast<PReal*>(power), divisor, acc)
   if (f.C == kFftElems / 2) {  // 2048-point rows, 128 threads
     NUS_ROWS(8, 128);
   } else if (r0 == 16) NUS_ROWS(16, kFftThreads);

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <utility>
 #include <cufft.h>
 
 #include <atomic>
@@ -216,6 +217,31 @@ void gpss_interpolated_device(const double* d_t, const double* h_t, int64_t n, d
 
 __host__ __device__ inline int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }
 __host__ __device__ inline int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+// ---- programmatic dependent launch ---------------------------------------------------
+// The per-spectrum kernels are launched with programmatic stream serialisation: a kernel's
+// CTAs may be dispatched while its predecessor drains, and each waits (griddepcontrol.wait:
+// predecessor complete, memory visible) before its first dependent read, so stream order is
+// unchanged; only launch latency and the predecessor's tail are overlapped.  Opt-in
+// (NUS_PDL=1): on C2 the early-dispatched CTAs held slots and the step got slower.
+bool pdl_enabled();
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  NUS_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
 
 // ---- double-double helpers ---------------------------------------------------
 

@@ -379,6 +379,8 @@ __global__ void __launch_bounds__(kTcWarps * 32, kTcCtasPerSm) spread_tc_kernel(
     reinterpret_cast<double2*>(mine)[i] = double2{0.0, 0.0};
   for (int i = lane; i < RS; i += 32) srel[i] = 1 << 20;  // absent points: outside every block
   __syncthreads();
+  pdl_launch_dependents();
+  pdl_wait();  // x (and the grid's previous reader) before any load or store
 
   const int stride = static_cast<int>(gridDim.x) * kTcWarps;
   TcPos p0{0, static_cast<int>(blockIdx.x) * kTcWarps + warp};
@@ -505,7 +507,7 @@ void launch_tc(const SpreadParams<Real>& P, cudaStream_t s) {
   }
   const int64_t warps = P.nseg_used * P.channels;
   const int64_t grid = std::min<int64_t>((warps + kTcWarps - 1) / kTcWarps, static_cast<int64_t>(blocks_per_sm) * sms);
-  spread_tc_kernel<Real, XK><<<static_cast<unsigned>(grid), kTcWarps * 32, smem, s>>>(P);
+  launch_pdl(spread_tc_kernel<Real, XK>, dim3(static_cast<unsigned>(grid)), dim3(kTcWarps * 32), smem, s, P);
   note_launch();
   check_launch("spread_tc_kernel");
 }
