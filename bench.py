@@ -214,6 +214,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--eps", type=float, default=None, help="override the workload's NUFFT tolerance")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -233,6 +234,8 @@ def main():
     dev = torch.device("cuda", local)
 
     wl = make_workload(args.workload, rank)
+    if args.eps is not None:
+        wl.eps = args.eps
     est = _Estimator(wl.times, wl.centers, wl.f_max, float(wl.f_w[0]), wl.k, wl.eps, 1,
                      wl.precision, local)
     setup = est.setup_ms()

@@ -54,6 +54,13 @@ enum nus_status {
 enum nus_path_policy { NUS_AUTO_SELECT = 0, NUS_FORCE_FAST = 1, NUS_FORCE_DIRECT = 2 };
 enum nus_path { NUS_PATH_DIRECT = 0, NUS_PATH_FAST = 1 };
 enum nus_precision { NUS_F64 = 0, NUS_F32 = 1 };
+/* Spreading kernel of the fast path.  GAUSSIAN is the reference's own kernel (support 2w,
+ * nufft.cpp:90-142): transforms replicate the reference to ~1e-12.  ES (exponential of
+ * semicircle, exp(beta (sqrt(1 - z^2) - 1)), support ns = 2 ceil(log10(10/eps) / 2) cells,
+ * beta = 2.30 ns) meets the same contract max|fast - direct| <= eps ||y||_1 with ~2.4x
+ * narrower support; it is the default.  Bins (nus_plan_first_cells) are the reference's
+ * either way. */
+enum nus_kernel { NUS_KERNEL_GAUSSIAN = 0, NUS_KERNEL_ES = 1 };
 
 typedef struct nus_plan_s* nus_plan_t;
 typedef struct nus_mtnufft_s* nus_mtnufft_t;
@@ -71,6 +78,8 @@ typedef struct {
   double tau;              /* Gaussian width (nufft.cpp:105-108) */
   double df;               /* centre spacing */
   double fshift;           /* f0 + (I/2) df */
+  int32_t kernel;          /* enum nus_kernel (fast path) */
+  int32_t support;         /* cells per sample actually spread: 2w (Gaussian) or ns (ES) */
 } nus_plan_info_t;
 
 const char* nus_last_error(void);
@@ -79,6 +88,10 @@ int nus_device_info(int device, int32_t* cc_major, int32_t* cc_minor, int32_t* s
                     int64_t* total_mem);
 /* Number of this library's kernels launched so far (process-wide). */
 int64_t nus_kernel_launch_count(void);
+/* Process-wide spreading kernel for plans created afterwards (enum nus_kernel).  The initial
+ * value is NUS_KERNEL_ES, or the NUS_KERNEL environment variable ("gaussian" / "es"). */
+int nus_set_spread_kernel(int32_t kind);
+int nus_get_spread_kernel(int32_t* kind);
 
 /* ---- NufftPlan (nufft.hpp:31-76) ---------------------------------------- */
 int nus_plan_create(const double* times, int64_t n, const double* centers, int64_t n_centers,

@@ -83,7 +83,8 @@ _i32p = ctypes.POINTER(ctypes.c_int32)
 class PlanInfo(ctypes.Structure):
     _fields_ = [("n_samples", _i64), ("n_centers", _i64), ("epsilon", _d), ("oversampling", _i32),
                 ("path", _i32), ("centers_uniform", _i32), ("precision", _i32),
-                ("spread_width", _i64), ("mr", _i64), ("tau", _d), ("df", _d), ("fshift", _d)]
+                ("spread_width", _i64), ("mr", _i64), ("tau", _d), ("df", _d), ("fshift", _d),
+                ("kernel", _i32), ("support", _i32)]
 
 
 class MtnufftConfig(ctypes.Structure):
@@ -97,6 +98,8 @@ _SIGS = {
     "nus_last_error": [],
     "nus_device_info": [ctypes.c_int, _i32p, _i32p, _i32p, _i64p],
     "nus_kernel_launch_count": [],
+    "nus_set_spread_kernel": [_i32],
+    "nus_get_spread_kernel": [_i32p],
     "nus_plan_create": [_dp, _i64, _dp, _i64, _d, _i32, _i32, _i32, _i32, ctypes.POINTER(_vp)],
     "nus_plan_destroy": [_vp],
     "nus_plan_info": [_vp, ctypes.POINTER(PlanInfo)],

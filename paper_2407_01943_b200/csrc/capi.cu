@@ -58,6 +58,8 @@ void fill_info(const nus::Plan& pl, nus_plan_info_t* info) {
   info->tau = p.tau;
   info->df = p.df;
   info->fshift = p.fshift;
+  info->kernel = p.kernel;
+  info->support = p.sw;
 }
 
 // Execute the transform of one complex vector already on the device.
@@ -88,6 +90,20 @@ extern "C" {
 const char* nus_last_error(void) { return g_last_error.c_str(); }
 
 int64_t nus_kernel_launch_count(void) { return nus::g_launches.load(); }
+
+int nus_set_spread_kernel(int32_t kind) {
+  return guarded([&] {
+    nus::require(kind == NUS_KERNEL_GAUSSIAN || kind == NUS_KERNEL_ES, "unknown spreading kernel");
+    nus::set_default_kernel(kind);
+  });
+}
+
+int nus_get_spread_kernel(int32_t* kind) {
+  return guarded([&] {
+    nus::require(kind != nullptr, "null output");
+    *kind = nus::default_kernel();
+  });
+}
 
 int nus_device_info(int device, int32_t* cc_major, int32_t* cc_minor, int32_t* sm_count,
                     int64_t* total_mem) {

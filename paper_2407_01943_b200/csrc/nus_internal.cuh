@@ -82,7 +82,35 @@ struct PlanParams {
   int64_t mode_offset = 0;
   double beta = 0;        // Gaussian exponent per cell^2: (2pi/Mr)^2 / (4 tau)
   double deconv_norm = 0; // sqrt(pi/tau)/Mr
+  // spreading kernel (fast path): NUS_KERNEL_GAUSSIAN (the reference's, sw = 2w) or
+  // NUS_KERNEL_ES (sw = ns cells); a point's support starts at cell j0 + sshift, j0 being
+  // the reference bin (nufft.cpp:118-121), sshift = w - ns/2 for ES, 0 for the Gaussian
+  int kernel = NUS_KERNEL_GAUSSIAN;
+  int sw = 0;
+  int sshift = 0;
+  double es_beta = 0;
 };
+
+// ---- exponential-of-semicircle kernel (es.cu) ----------------------------------------
+// phi(z) = exp(beta (sqrt(1 - z^2) - 1)) on |z| <= 1, z = 2 (cell - position) / ns.
+constexpr int kEsMinNs = 4, kEsMaxNs = 16;
+int default_kernel();
+void set_default_kernel(int kind);
+int es_width(double eps);                 // ns: even, 4 .. 16
+inline double es_beta(int ns) { return 2.30 * ns; }
+// Monomial coefficients (in s = 2 fr - 1, degree ns + 1) of the weight of cell p = 0..ns-1 of
+// a point at fractional offset fr in [0, 1): out[p * (ns + 2) + d].
+void es_fit(int ns, double* out);
+// Offset of ns's block in the packed table of all even ns in [kEsMinNs, kEsMaxNs].
+__host__ __device__ constexpr int es_table_offset(int ns) {
+  int o = 0;
+  for (int q = kEsMinNs; q < ns; q += 2) o += q * (q + 2);
+  return o;
+}
+constexpr int kEsTableSize = es_table_offset(kEsMaxNs + 2);
+// Gauss-Legendre rule for Phi(m) = ns int_0^{pi/2} e^{beta (cos th - 1)} cos(a sin th) cos th dth:
+// node pairs (sin th_q, w_q e^{beta (cos th_q - 1)} cos th_q), q < nq.
+void es_quadrature(int ns, int nq, double* pairs);
 
 struct SpreadTables {
   int tile = 128;               // cells per spreading tile (= spread.cu kTile)

@@ -124,6 +124,15 @@ void plan_validate_and_select(PlanParams& p, const double* centers, int64_t nc, 
                    : NUS_PATH_DIRECT;
   }
   p.w = static_cast<int>(std::max<int64_t>(4, static_cast<int64_t>(std::ceil(0.55 * (-std::log(eps))))));
+  p.kernel = default_kernel();
+  if (p.kernel == NUS_KERNEL_ES) {
+    p.sw = es_width(eps);
+    p.sshift = p.w - p.sw / 2;
+    p.es_beta = es_beta(p.sw);
+  } else {
+    p.sw = 2 * p.w;
+    p.sshift = 0;
+  }
   if (p.path != NUS_PATH_FAST) return;
   // nufft.cpp:96-114, same operation order
   p.f0 = centers[0];
@@ -147,7 +156,7 @@ namespace {
 // radix-sort key/value.  Explicit _rn intrinsics forbid FMA contraction so the
 // IEEE operation order matches the reference TU (compiled without -mfma).
 __global__ void bins_kernel(const double* __restrict__ t, int64_t n, int64_t total, double neg2pi_df,
-                            double mr_d, int64_t mr, int w, int mr_bits, int64_t* __restrict__ j0_out,
+                            double mr_d, int64_t mr, int w, int sshift, int mr_bits, int64_t* __restrict__ j0_out,
                             uint64_t* __restrict__ keys, int32_t* __restrict__ vals) {
   const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (g >= total) return;
@@ -158,7 +167,7 @@ __global__ void bins_kernel(const double* __restrict__ t, int64_t n, int64_t tot
   const double cell = __ddiv_rn(__dmul_rn(x, mr_d), kTwoPi);
   const int64_t j0 = static_cast<int64_t>(floor(cell)) - w + 1;
   j0_out[g] = j0;
-  int64_t s = j0 % mr;
+  int64_t s = (j0 + sshift) % mr;  // the spreading window's first cell
   if (s < 0) s += mr;
   keys[g] = (static_cast<uint64_t>(c) << mr_bits) | static_cast<uint64_t>(s);
   vals[g] = static_cast<int32_t>(i);
@@ -170,7 +179,7 @@ __global__ void sorted_tables_kernel(const double* __restrict__ t, int64_t n, in
                                      const uint64_t* __restrict__ keys_sorted,
                                      const int32_t* __restrict__ perm, int mr_bits,
                                      double neg2pi_df, double neg2pi_fshift, double mr_d,
-                                     double beta, int w2, int32_t* __restrict__ start,
+                                     double beta, int w2, int es, int32_t* __restrict__ start,
                                      Real* __restrict__ gauss, Real* __restrict__ prephase) {
   const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (g >= total) return;
@@ -185,9 +194,14 @@ __global__ void sorted_tables_kernel(const double* __restrict__ t, int64_t n, in
   // Gaussian factors around the support centre, fr' = frac - 1/2:
   //   exp(-beta (frac + w - 1 - p)^2) = A g^p C_p,  g = e^{2 beta fr'},
   //   A = e^{-beta fr' (fr' + 2w - 1)},  C_p = e^{-beta (p - w + 1/2)^2}
+  if (es) {  // ES: the spread evaluates the window polynomials at fr
+    gauss[2 * g] = static_cast<Real>(fr);
+    gauss[2 * g + 1] = Real(0);
+  } else {
   const double frc = fr - 0.5;
   gauss[2 * g] = static_cast<Real>(exp(-beta * frc * (frc + static_cast<double>(w2 - 1))));
   gauss[2 * g + 1] = static_cast<Real>(exp(2.0 * beta * frc));
+  }
   double sn, cs;
   sincos(__dmul_rn(neg2pi_fshift, tv), &sn, &cs);  // nufft.cpp:116-117
   prephase[2 * g] = static_cast<Real>(cs);
@@ -259,6 +273,23 @@ __global__ void deconv_kernel(int64_t nc, int64_t mode_offset, double tau, doubl
   out[i] = static_cast<Real>(norm * exp(tau * m * m));  // nufft.cpp:139
 }
 
+// ES deconvolution: 1 / Phi(m), Phi(m) = int phi(2u/ns) cos(2 pi u m / Mr) du over the support
+// (cell units), by the Gauss-Legendre rule of es_quadrature (pairs (sin th_q, weight_q)).
+constexpr int kEsQuad = 100;
+template <typename Real>
+__global__ void deconv_es_kernel(int64_t nc, int64_t mode_offset, double a_per_mode, double ns,
+                                 const double* __restrict__ pairs, Real* __restrict__ out) {
+  __shared__ double sq[2 * kEsQuad];
+  for (int q = threadIdx.x; q < 2 * kEsQuad; q += blockDim.x) sq[q] = pairs[q];
+  __syncthreads();
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= nc) return;
+  const double a = a_per_mode * static_cast<double>(i - mode_offset);
+  double phi = 0.0;
+  for (int q = 0; q < kEsQuad; ++q) phi += sq[2 * q + 1] * cos(a * sq[2 * q]);
+  out[i] = static_cast<Real>(1.0 / (ns * phi));
+}
+
 int log2_exact(int64_t v) {
   int b = 0;
   while ((int64_t{1} << b) < v) ++b;
@@ -291,7 +322,7 @@ void plan_build_tables(Plan& plan, cudaStream_t st) {
   const int threads = 256;
   const unsigned blocks = static_cast<unsigned>((total + threads - 1) / threads);
   bins_kernel<<<blocks, threads, 0, st>>>(plan.d_times.as<double>(), p.n, total, neg2pi_df, mr_d,
-                                          p.mr, p.w, mr_bits, tb.first_cell.as<int64_t>(),
+                                          p.mr, p.w, p.sshift, mr_bits, tb.first_cell.as<int64_t>(),
                                           keys.as<uint64_t>(), vals.as<int32_t>());
   note_launch();
   check_launch("bins_kernel");
@@ -312,25 +343,25 @@ void plan_build_tables(Plan& plan, cudaStream_t st) {
   if (p.precision == NUS_F64)
     sorted_tables_kernel<double><<<blocks, threads, 0, st>>>(
         plan.d_times.as<double>(), p.n, total, keys_sorted.as<uint64_t>(), tb.perm.as<int32_t>(),
-        mr_bits, neg2pi_df, neg2pi_fshift, mr_d, p.beta, 2 * p.w, tb.start.as<int32_t>(),
+        mr_bits, neg2pi_df, neg2pi_fshift, mr_d, p.beta, p.sw, p.kernel == NUS_KERNEL_ES, tb.start.as<int32_t>(),
         tb.gauss.as<double>(), tb.prephase.as<double>());
   else
     sorted_tables_kernel<float><<<blocks, threads, 0, st>>>(
         plan.d_times.as<double>(), p.n, total, keys_sorted.as<uint64_t>(), tb.perm.as<int32_t>(),
-        mr_bits, neg2pi_df, neg2pi_fshift, mr_d, p.beta, 2 * p.w, tb.start.as<int32_t>(),
+        mr_bits, neg2pi_df, neg2pi_fshift, mr_d, p.beta, p.sw, p.kernel == NUS_KERNEL_ES, tb.start.as<int32_t>(),
         tb.gauss.as<float>(), tb.prephase.as<float>());
   note_launch();
   check_launch("sorted_tables_kernel");
 
   tb.tile = static_cast<int>(std::min<int64_t>(128, p.mr));  // = spread.cu kTile
-  require(tb.tile >= 2 * p.w, "NufftPlan: spread width exceeds the tile size");
+  require(tb.tile >= p.sw, "NufftPlan: spread width exceeds the tile size");
   tb.ntiles = p.mr / tb.tile;
   tb.tile_range.alloc(p.channels * (tb.ntiles + 1) * 2 * sizeof(int32_t));
   tb.wrap_lo.alloc(p.channels * sizeof(int32_t));
   {
     const int64_t cnt = p.channels * (tb.ntiles + 1);
     tile_ranges_kernel<<<static_cast<unsigned>((cnt + 255) / 256), 256, 0, st>>>(
-        tb.start.as<int32_t>(), p.n, p.channels, tb.ntiles, tb.tile, 2 * p.w, p.mr,
+        tb.start.as<int32_t>(), p.n, p.channels, tb.ntiles, tb.tile, p.sw, p.mr,
         tb.tile_range.as<int32_t>(), tb.wrap_lo.as<int32_t>());
     note_launch();
     check_launch("tile_ranges_kernel");
@@ -340,12 +371,27 @@ void plan_build_tables(Plan& plan, cudaStream_t st) {
   {
     const int64_t cnt = p.channels * tb.nseg;
     seg_ranges_kernel<<<static_cast<unsigned>((cnt + 255) / 256), 256, 0, st>>>(
-        tb.start.as<int32_t>(), p.n, p.channels, tb.nseg, 2 * p.w, p.mr, tb.seg_range.as<int32_t>());
+        tb.start.as<int32_t>(), p.n, p.channels, tb.nseg, p.sw, p.mr, tb.seg_range.as<int32_t>());
     note_launch();
     check_launch("seg_ranges_kernel");
   }
   tb.deconv.alloc(p.nc * rs);
-  if (p.precision == NUS_F64)
+  if (p.kernel == NUS_KERNEL_ES) {
+    std::vector<double> pairs(2 * kEsQuad);
+    es_quadrature(p.sw, kEsQuad, pairs.data());
+    DeviceBuffer dq(pairs.size() * sizeof(double));
+    NUS_CUDA(cudaMemcpyAsync(dq.ptr, pairs.data(), dq.bytes, cudaMemcpyHostToDevice, st));
+    const double a_per_mode = kPi * static_cast<double>(p.sw) / static_cast<double>(p.mr);
+    if (p.precision == NUS_F64)
+      deconv_es_kernel<double><<<static_cast<unsigned>((p.nc + 255) / 256), 256, 0, st>>>(
+          p.nc, p.mode_offset, a_per_mode, static_cast<double>(p.sw), dq.as<double>(), tb.deconv.as<double>());
+    else
+      deconv_es_kernel<float><<<static_cast<unsigned>((p.nc + 255) / 256), 256, 0, st>>>(
+          p.nc, p.mode_offset, a_per_mode, static_cast<double>(p.sw), dq.as<double>(), tb.deconv.as<float>());
+    note_launch();
+    check_launch("deconv_es_kernel");
+    NUS_CUDA(cudaStreamSynchronize(st));  // dq is released at scope end
+  } else if (p.precision == NUS_F64)
     deconv_kernel<double><<<static_cast<unsigned>((p.nc + 255) / 256), 256, 0, st>>>(
         p.nc, p.mode_offset, p.tau, p.deconv_norm, tb.deconv.as<double>());
   else
@@ -365,7 +411,7 @@ void plan_build_tables(Plan& plan, cudaStream_t st) {
     NUS_CUDA(cudaMemsetAsync(occ.ptr, 0, occ.bytes, st));
     const int64_t total = p.channels * p.n;
     row_occupancy_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(
-        tb.start.as<int32_t>(), total, 2 * p.w, p.mr, ff.lgC, occ.as<uint8_t>());
+        tb.start.as<int32_t>(), total, p.sw, p.mr, ff.lgC, occ.as<uint8_t>());
     note_launch();
     check_launch("row_occupancy_kernel");
     std::vector<uint8_t> h(ff.R);

@@ -24,6 +24,8 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <vector>
 
 #include "nus_internal.cuh"
 
@@ -312,7 +314,9 @@ __device__ inline void tc_advance(TcCursor& u, int4& pre, TcPos& pp, const Sprea
     return;
   }
   u.nb = min(32, u.hi - u.b0);
-  u.last = u.b0 + 32 >= u.hi && u.part == 1;
+  // the segment's final round: the last of part 1, or of part 0 when it has no own points
+  // (a multi-round part 0 of an own-empty segment must still write its cells)
+  u.last = u.b0 + 32 >= u.hi && (u.part == 1 || u.own_hi <= u.own_lo);
 }
 
 // x kinds (template XK): 0 f64 real, 1 f64 complex, 2 f32 real, 3 f32 complex
@@ -361,7 +365,13 @@ __device__ inline int tc_perm(const TcCursor& u, int lane, const SpreadParams<Re
   return (u.valid && lane < u.nb) ? P.perm[static_cast<int64_t>(u.c) * P.n + u.b0 + lane] : 0;
 }
 
-template <typename Real, int XK>
+// ES window polynomials of every even ns (es.cu es_fit), uploaded once per device: with ns a
+// template parameter every coefficient is a constant-bank operand of its DFMA.
+__constant__ double c_es[kEsTableSize];
+
+// NS = 0: the reference's Gaussian (support P.w2, geometric chains); NS > 0: the ES window on NS
+// cells, weight of cell p = Horner(c_es[ns block][p], 2 fr - 1).
+template <typename Real, int XK, int NS>
 __global__ void __launch_bounds__(kTcWarps * 32, kTcCtasPerSm) spread_tc_kernel(const SpreadParams<Real> P) {
   using R2 = typename Vec2<Real>::T;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -374,7 +384,9 @@ __global__ void __launch_bounds__(kTcWarps * 32, kTcCtasPerSm) spread_tc_kernel(
   double* sw = reinterpret_cast<double*>(sz + 8 * RS);   // W [kTcPts points][RS], slot = cell mod 32
   int* srel = reinterpret_cast<int*>(sw + kTcPts * RS);  // rel [RS points]
 
-  for (int i = threadIdx.x; i < P.w2; i += blockDim.x) scq[i] = static_cast<double>(P.cq[i]);
+  const int w2 = NS > 0 ? NS : P.w2;
+  if constexpr (NS == 0)
+    for (int i = threadIdx.x; i < P.w2; i += blockDim.x) scq[i] = static_cast<double>(P.cq[i]);
   for (int i = lane; i < static_cast<int>((kWarpBytes - RS * sizeof(int)) / 16); i += 32)
     reinterpret_cast<double2*>(mine)[i] = double2{0.0, 0.0};
   for (int i = lane; i < RS; i += 32) srel[i] = 1 << 20;  // absent points: outside every block
@@ -431,7 +443,20 @@ __global__ void __launch_bounds__(kTcWarps * 32, kTcCtasPerSm) spread_tc_kernel(
         if (k < P.kg) sz[k * RS + lane] = double2{wk * yr, wk * yi};
       }
       srel[lane] = rel;
-      if (has) {  // W_p = A g^p C_p stored at slot (rel + p) mod 32 of the point's row;
+      if constexpr (NS > 0) {
+        if (has) {
+          const double sv = 2.0 * static_cast<double>(pt.ag.x) - 1.0;
+          double* row = sw + lane * RS;
+#pragma unroll
+          for (int p = 0; p < NS; ++p) {
+            const double* cf = c_es + es_table_offset(NS) + p * (NS + 2);
+            double v = cf[NS + 1];
+#pragma unroll
+            for (int d = NS; d >= 0; --d) v = fma(v, sv, cf[d]);
+            row[(rel + p) & 31] = v;
+          }
+        }
+      } else if (has) {  // W_p = A g^p C_p stored at slot (rel + p) mod 32 of the point's row;
                   // C_{p+2}/C_p = e^{-4 beta (p - w + 1.5)} is a geometric chain too
         const double gg = static_cast<double>(pt.ag.y), g2 = gg * gg, A = static_cast<double>(pt.ag.x);
         double ae = A * P.c0, ao = A * gg * P.c1, qe = g2 * P.qe0, qo = g2 * P.qo0;
@@ -457,12 +482,12 @@ __global__ void __launch_bounds__(kTcWarps * 32, kTcCtasPerSm) spread_tc_kernel(
     const int* rcol = srel + t;
 #pragma unroll
     for (int b = 0; b < 4 && busy; ++b) {
-      const int lo = __popc(__ballot_sync(0xffffffffu, rel < 8 * b - (P.w2 - 1)));
+      const int lo = __popc(__ballot_sync(0xffffffffu, rel < 8 * b - (w2 - 1)));
       const int hi = __popc(__ballot_sync(0xffffffffu, rel < 8 * b + 8));
       for (int p0 = lo; p0 < hi; p0 += 4) {  // rows up to hi + 3 <= 34: absent ones are masked
         const int pp = 8 * b + g - rcol[p0];
         const double wv = wrow[p0 * RS + 8 * b];
-        const double a = static_cast<unsigned>(pp) < static_cast<unsigned>(P.w2) ? wv : 0.0;
+        const double a = static_cast<unsigned>(pp) < static_cast<unsigned>(w2) ? wv : 0.0;
         const double2 zb = zcol[p0];
         dmma_8x8x4(cr[b][0], cr[b][1], a, zb.x);
         dmma_8x8x4(ci[b][0], ci[b][1], a, zb.y);
@@ -489,25 +514,39 @@ __global__ void __launch_bounds__(kTcWarps * 32, kTcCtasPerSm) spread_tc_kernel(
   }
 }
 
-template <typename Real, int XK>
+void es_upload() {  // once per device
+  static std::mutex mu;
+  static bool done[64] = {};
+  int dev = 0;
+  NUS_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 64 && done[dev]) return;
+  std::vector<double> tab(kEsTableSize);
+  for (int ns = kEsMinNs; ns <= kEsMaxNs; ns += 2) es_fit(ns, tab.data() + es_table_offset(ns));
+  NUS_CUDA(cudaMemcpyToSymbol(c_es, tab.data(), tab.size() * sizeof(double)));
+  if (dev < 64) done[dev] = true;
+}
+
+template <typename Real, int XK, int NS>
 void launch_tc(const SpreadParams<Real>& P, cudaStream_t s) {
   const size_t warp_bytes =
       (8 * kTcRows) * sizeof(double2) + (kTcPts * kTcRows) * sizeof(double) + kTcRows * sizeof(int);
   const size_t smem = kMaxW2 * sizeof(double) + kTcWarps * warp_bytes;
   static int blocks_per_sm = 0, sms = 0;
   if (blocks_per_sm == 0) {
-    NUS_CUDA(cudaFuncSetAttribute(spread_tc_kernel<Real, XK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    NUS_CUDA(cudaFuncSetAttribute(spread_tc_kernel<Real, XK, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
     int dev = 0;
     NUS_CUDA(cudaGetDevice(&dev));
     NUS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    NUS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, spread_tc_kernel<Real, XK>,
+    NUS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, spread_tc_kernel<Real, XK, NS>,
                                                            kTcWarps * 32, smem));
     require(blocks_per_sm > 0, "spread: tensor-core kernel does not fit on an SM");
   }
   const int64_t warps = P.nseg_used * P.channels;
   const int64_t grid = std::min<int64_t>((warps + kTcWarps - 1) / kTcWarps, static_cast<int64_t>(blocks_per_sm) * sms);
-  launch_pdl(spread_tc_kernel<Real, XK>, dim3(static_cast<unsigned>(grid)), dim3(kTcWarps * 32), smem, s, P);
+  if constexpr (NS > 0) es_upload();
+  launch_pdl(spread_tc_kernel<Real, XK, NS>, dim3(static_cast<unsigned>(grid)), dim3(kTcWarps * 32), smem, s, P);
   note_launch();
   check_launch("spread_tc_kernel");
 }
@@ -515,8 +554,23 @@ void launch_tc(const SpreadParams<Real>& P, cudaStream_t s) {
 __device__ double g_one_f64 = 1.0;
 __device__ float g_one_f32 = 1.0f;
 
+template <typename Real, int XK>
+void launch_tc_ns(const SpreadParams<Real>& P, int ns, cudaStream_t s) {
+  switch (ns) {
+    case 0: launch_tc<Real, XK, 0>(P, s); break;
+    case 4: launch_tc<Real, XK, 4>(P, s); break;
+    case 6: launch_tc<Real, XK, 6>(P, s); break;
+    case 8: launch_tc<Real, XK, 8>(P, s); break;
+    case 10: launch_tc<Real, XK, 10>(P, s); break;
+    case 12: launch_tc<Real, XK, 12>(P, s); break;
+    case 14: launch_tc<Real, XK, 14>(P, s); break;
+    case 16: launch_tc<Real, XK, 16>(P, s); break;
+    default: fail(NUS_ERR_INVALID_ARGUMENT, "spread: unsupported ES width");
+  }
+}
+
 template <typename Real>
-void launch_tc_x(SpreadParams<Real> P, cudaStream_t s) {
+void launch_tc_x(SpreadParams<Real> P, int ns, cudaStream_t s) {
   if (P.tapers) {
     P.taper_base = P.tapers;
     P.tstride_k = P.n;
@@ -531,10 +585,10 @@ void launch_tc_x(SpreadParams<Real> P, cudaStream_t s) {
   }
   const int xk = P.x_dtype == 0 ? (P.x_complex ? 1 : 0) : (P.x_complex ? 3 : 2);
   switch (xk) {
-    case 0: launch_tc<Real, 0>(P, s); break;
-    case 1: launch_tc<Real, 1>(P, s); break;
-    case 2: launch_tc<Real, 2>(P, s); break;
-    default: launch_tc<Real, 3>(P, s); break;
+    case 0: launch_tc_ns<Real, 0>(P, ns, s); break;
+    case 1: launch_tc_ns<Real, 1>(P, ns, s); break;
+    case 2: launch_tc_ns<Real, 2>(P, ns, s); break;
+    default: launch_tc_ns<Real, 3>(P, ns, s); break;
   }
 }
 
@@ -559,7 +613,7 @@ void spread_typed(const Plan& plan, const SpreadArgs& a, cudaStream_t s) {
   const PlanParams& p = plan.p;
   const SpreadTables& tb = plan.tab;
   require(tb.tile == kTile || p.mr < kTile, "spread: unexpected tile size");
-  require(2 * p.w <= kMaxW2, "spread: spread width too large");
+  require(p.sw <= kMaxW2, "spread: spread width too large");
   SpreadParams<Real> P{};
   P.start = tb.start.as<int32_t>();
   P.perm = tb.perm.as<int32_t>();
@@ -599,7 +653,7 @@ void spread_typed(const Plan& plan, const SpreadArgs& a, cudaStream_t s) {
   P.s1 = a.s1 < 0 ? p.n : a.s1;
   P.tile = tb.tile;
   P.w = p.w;
-  P.w2 = 2 * p.w;
+  P.w2 = p.sw;
   P.x_dtype = a.x_dtype;
   P.x_complex = a.x_complex ? 1 : 0;
   P.beta = static_cast<Real>(p.beta);
@@ -623,6 +677,8 @@ void spread_typed(const Plan& plan, const SpreadArgs& a, cudaStream_t s) {
     const char* e = std::getenv("NUS_SPREAD");
     return !(e && std::strcmp(e, "gather") == 0);
   }();
+  require(use_tc || p.kernel == NUS_KERNEL_GAUSSIAN, "spread: the gather kernel implements the Gaussian only");
+  const int ns = p.kernel == NUS_KERNEL_ES ? p.sw : 0;
   // taper groups of at most 8, balanced
   const int64_t k = a.tapers ? a.k : 1;
   const int64_t groups = (k + 7) / 8;
@@ -632,7 +688,7 @@ void spread_typed(const Plan& plan, const SpreadArgs& a, cudaStream_t s) {
     P.k0 = static_cast<int>(k0);
     P.kg = static_cast<int>(kg);
     if (use_tc) {
-      launch_tc_x<Real>(P, s);
+      launch_tc_x<Real>(P, ns, s);
       k0 += kg;
       continue;
     }

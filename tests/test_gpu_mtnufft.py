@@ -11,7 +11,7 @@ import pytest
 
 import paper_2407_01943_b200 as nus
 from paper_2407_01943_b200 import workloads as W
-from conftest import golden, rel_l2, sign_align
+from conftest import KERNELS, golden, kernel_tol, rel_l2, sign_align
 from oracle import C, REF, ref_available
 
 pytestmark = pytest.mark.gpu
@@ -25,8 +25,10 @@ def estimator(wl, tapers=None, precision=None, k=None, eps=None, policy=nus.Nuff
     return nus.MtnufftEstimator(nus.SamplingGrid(t), nus.SignalBand(wl.f_max), plan, opts, tapers=tapers)
 
 
-def test_c1_full_pipeline_vs_reference_oracle_a():
-    """Config C1 end to end (GPU DPSS + spline + R(B) + NUFFT) vs the full reference estimator."""
+@pytest.mark.parametrize("kern", KERNELS)
+def test_c1_full_pipeline_vs_reference_oracle_a(kern):
+    """Config C1 end to end (GPU DPSS + spline + R(B) + NUFFT) vs the full reference estimator,
+    under the reference's Gaussian window and under the ES window."""
     g = golden("c1.npz")
     wl = W.c1()
     assert np.array_equal(wl.times, g["t"]) and np.array_equal(wl.values, g["x"])
@@ -35,23 +37,27 @@ def test_c1_full_pipeline_vs_reference_oracle_a():
     assert rel_l2(p, g["power"]) <= 1e-6
     w = est.tapers().weights_matrix()
     assert np.abs(sign_align(w, g["tapers"]) - g["tapers"]).max() < 1e-6 * np.abs(g["tapers"]).max()
-    # with the reference's own tapers injected, the NUFFT stage agrees to ~1e-12
+    # with the reference's own tapers injected, the NUFFT stage agrees to ~1e-12 (Gaussian, the
+    # reference's own window) / ~eps (ES: a different window meeting the same eps contract)
     p_inj = estimator(wl, tapers=g["tapers"]).estimate(wl.values).power
-    assert rel_l2(p_inj, g["power"]) < 1e-11
+    assert rel_l2(p_inj, g["power"]) < kernel_tol(kern, 1e-11, 1e-8)
     assert np.array_equal(est.estimate(wl.values).flags, g["flags"])
 
 
-def test_c1_fp32_mode():
+@pytest.mark.parametrize("kern", KERNELS)
+def test_c1_fp32_mode(kern):
     g = golden("c1.npz")
     wl = W.c1()
     p = estimator(wl, tapers=g["tapers"], precision="f32", eps=1e-5).estimate(wl.values).power
     assert rel_l2(p, g["power"]) <= 1e-4
 
 
-@pytest.fixture(scope="module")
-def c2_case():
+@pytest.fixture(scope="module", params=KERNELS)
+def c2_case(request):
     wl = W.c2()
-    est = estimator(wl)
+    with nus.spread_kernel(request.param):
+        est = estimator(wl)
+    assert nus.SpreadKernel(est.transform_info().kernel).name == request.param
     w = est.tapers().weights_matrix()
     ref = C.mtnufft_power(wl.times, w, wl.values, wl.centers, 1e-9)  # Oracle-B (restatement)
     return wl, est, w, ref
@@ -61,12 +67,14 @@ def test_c2_fp64_vs_oracle(c2_case):
     wl, est, w, ref = c2_case
     p = est.estimate(wl.values).power
     assert rel_l2(p, ref) <= 1e-6
-    assert rel_l2(p, ref) < 1e-8  # the NUFFT stage is far tighter than the spec
+    kern = nus.SpreadKernel(est.transform_info().kernel).name
+    assert rel_l2(p, ref) < kernel_tol(kern, 1e-8, 2e-8)  # the NUFFT stage is far tighter than the spec
 
 
 def test_c2_fp32_vs_fp64_oracle(c2_case):
-    wl, _, w, ref = c2_case
-    est32 = estimator(wl, tapers=w, precision="f32", eps=1e-5)
+    wl, est, w, ref = c2_case
+    with nus.spread_kernel(nus.SpreadKernel(est.transform_info().kernel)):
+        est32 = estimator(wl, tapers=w, precision="f32", eps=1e-5)
     p = est32.estimate(wl.values).power
     assert rel_l2(p, ref) <= 1e-4
 
@@ -101,7 +109,8 @@ def test_c2_linearity_and_power_properties_full_size(c2_case):
     np.testing.assert_allclose(np.mean(np.abs(jx) ** 2, axis=0), p, rtol=1e-12)
 
 
-def test_c3_channels_batch_fp32():
+@pytest.mark.parametrize("kern", KERNELS)
+def test_c3_channels_batch_fp32(kern):
     wl = W.c3(channels=4, n=1 << 16)
     pl = nus.api._Estimator(wl.times, wl.centers, wl.f_max, float(wl.f_w[0]), wl.k, wl.eps, 0, "f32", 0)
     # per-channel tapers: the batch estimator builds each channel's tapers on its own grid
@@ -115,7 +124,8 @@ def test_c3_channels_batch_fp32():
         assert rel_l2(p[c], single.power(wl.values[c])[0]) <= 1e-4
 
 
-def test_c5_subset_vs_direct_nudft():
+@pytest.mark.parametrize("kern", KERNELS)
+def test_c5_subset_vs_direct_nudft(kern):
     """C5 check: N=2^14 subset as its own grid, MTNUFFT P vs exact direct-sum P."""
     full = W.c5(n=1 << 16)
     t, x = full.times[: 1 << 14], full.values[: 1 << 14]
@@ -133,15 +143,23 @@ def test_c5_subset_vs_direct_nudft():
     assert rel_l2(jd[0][::64], jc) < 1e-12
 
 
+@pytest.mark.parametrize("kern", KERNELS)
 @pytest.mark.parametrize("k,eps", [(1, 1e-3), (3, 1e-6), (15, 1e-9), (31, 1e-12)])
-def test_taper_count_and_width_sweep(k, eps):
-    """C5-style lattice over K (1..31, taper groups of 8) and eps (w = 4..16)."""
+def test_taper_count_and_width_sweep(k, eps, kern):
+    """C5-style lattice over K (1..31, taper groups of 8) and eps (w = 4..16; ES ns = 4..14).
+    Gaussian: the reference's transform replicated; ES: P within the eps contract of the
+    exact direct-sum P (and of the reference's Gaussian P)."""
     wl = W.small(n=6000, n_centers=4096, k=k, nw=(k + 1) / 2, eps=eps, seed=k)
     est = estimator(wl)
     p = est.estimate(wl.values).power
     w = est.tapers().weights_matrix()
     ref = C.mtnufft_power(wl.times, w, wl.values, wl.centers, eps)
-    assert rel_l2(p, ref) < 1e-10
+    if kern == "gaussian":
+        assert rel_l2(p, ref) < 1e-10
+    else:
+        exact = C.mtnufft_power(wl.times, w, wl.values, wl.centers, eps, policy=2)
+        assert rel_l2(p, exact) < 10 * eps
+        assert rel_l2(p, ref) < 10 * eps
 
 
 def test_direct_path_estimator_small_problem():
