@@ -5,7 +5,7 @@ ARCH     := -gencode arch=compute_100a,code=sm_100a
 PKG      := paper_2407_01943_b200
 SRC      := $(PKG)/csrc
 LIBDIR   := $(PKG)/lib
-CU_SRCS  := $(SRC)/plan.cu $(SRC)/es.cu $(SRC)/spread.cu $(SRC)/fft.cu $(SRC)/transform.cu $(SRC)/tapers.cu $(SRC)/mtnufft.cu $(SRC)/ftest.cu $(SRC)/gep.cu $(SRC)/capi.cu
+CU_SRCS  := $(SRC)/plan.cu $(SRC)/es.cu $(SRC)/spread.cu $(SRC)/fft.cu $(SRC)/transform.cu $(SRC)/tapers.cu $(SRC)/normalise.cu $(SRC)/mtnufft.cu $(SRC)/ftest.cu $(SRC)/gep.cu $(SRC)/capi.cu
 CU_OBJS  := $(patsubst $(SRC)/%.cu,build/cu/%.o,$(CU_SRCS))
 NVFLAGS  := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC \
             --expt-relaxed-constexpr -Iinclude -I$(SRC) -Xptxas -warn-spills

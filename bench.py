@@ -59,6 +59,8 @@ def make_workload(name, rank):
         return W.c3(channels=int(os.environ.get("NUS_C3_CHANNELS", "32")), first_channel=32 * rank)
     if name == "c5":
         return W.c5()
+    if name == "c4":
+        return W.c4()
     if name == "c1":
         return W.c1()
     raise SystemExit(f"unknown workload {name}")
@@ -72,6 +74,7 @@ def describe(wl, name):
         "c3": f"c3: {wl.channels} channels x N=2^{int(np.log2(n))}, I=2^{int(np.log2(i))}, K={wl.k}, eps={wl.eps:g}, fp32",
         "c5": f"c5: jittered N=2^{int(np.log2(n))}, I=2^{int(np.log2(i))}, K={wl.k}, eps={wl.eps:g}, {wl.precision}",
         "c1": f"c1: N={n}, I={i}, K={wl.k}, eps={wl.eps:g}",
+        "c4": f"c4: clustered N=2^{int(np.log2(n))} (400 windows), I=2^{int(np.log2(i))}, K={wl.k} (NW={wl.nw:g}), eps={wl.eps:g}, {wl.precision}, all samples on one GPU",
     }[name]
     return desc
 
@@ -210,7 +213,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=20)
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c2f32", "c3", "c5"])
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c2f32", "c3", "c4", "c5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--e2e-steps", type=int, default=None)

@@ -151,6 +151,11 @@ int nus_tridiagonal_eigen(const double* diag, const double* offdiag, int64_t n, 
 int nus_signal_band_quadform(const double* times, int64_t n, double f_max, const double* w_host,
                              int64_t k, int64_t row_begin, int64_t row_end, int32_t device,
                              double* q_host);
+/* The same q_k in O(N log N) (normalise.cu): q = int_{-F}^{F} |W_k(f)|^2 df as a windowed lattice
+ * sum of the path's own type-1 NUFFT.  gpss_interpolated uses it above NUS_QUADFORM_EXACT_MAX
+ * samples (default 2^18; NUS_NORMALISE=exact|fast forces one form). */
+int nus_signal_band_quadform_fast(const double* times, int64_t n, double f_max, const double* w_host,
+                                  int64_t k, int32_t device, double* q_host);
 /* Un-normalised interpolated DPSS: spline of dpss_uniform(n, f_w*h*n, k) at t (tapers.cpp:156-174). */
 int nus_taper_spline(const double* times, int64_t n, double f_max, double f_w, int64_t k,
                      int32_t device, double* w_host);

@@ -113,6 +113,7 @@ _SIGS = {
     "nus_dpss": [_i64, _d, _i64, _i32, _dp, _dp, _dp],
     "nus_tridiagonal_eigen": [_dp, _dp, _i64, _i64, _i32, _dp, _dp, _dp],
     "nus_signal_band_quadform": [_dp, _i64, _d, _dp, _i64, _i64, _i64, _i32, _dp],
+    "nus_signal_band_quadform_fast": [_dp, _i64, _d, _dp, _i64, _i32, _dp],
     "nus_taper_spline": [_dp, _i64, _d, _d, _i64, _i32, _dp],
     "nus_gpss_interpolated": [_dp, _i64, _d, _d, _i64, _i32, _dp],
     "nus_mtnufft_create": [ctypes.POINTER(MtnufftConfig), _dp, _dp, _dp, ctypes.POINTER(_vp)],

@@ -25,7 +25,7 @@ __all__ = [
     "SamplingGrid", "SignalSeries", "SignalBand", "AnalysisBand", "BandPlan", "make_band_plan",
     "band_near_boundary", "NufftPath", "NufftPathPolicy", "NufftPlan", "ndft_direct", "nufft_fast",
     "DpssSet", "dpss_uniform", "tridiagonal_eigen", "TaperSet", "gpss_interpolated",
-    "signal_band_quadform", "EigenCoefficients", "eigencoefficients", "SpectrumEstimate",
+    "signal_band_quadform", "signal_band_quadform_fast", "EigenCoefficients", "eigencoefficients", "SpectrumEstimate",
     "MtnufftEstimator", "estimate_mtnufft", "default_taper_count", "kBandBoundary", "kBandFailed",
     "NusError", "InvalidArgument", "PlanMismatch", "BandRangeError", "ExtrapolationError",
     "NumericError", "NoDeviceError", "Precision", "DegenerateTapers", "FTestResult", "FTestOptions",
@@ -451,6 +451,17 @@ def signal_band_quadform(grid: SamplingGrid, band: SignalBand, w, rows=None, dev
     q = np.empty(w.shape[0])
     C.check(C.lib().nus_signal_band_quadform(C.dptr(t), t.size, band.f_max, C.dptr(w), w.shape[0],
                                              r0, r1, device, C.dptr(q)))
+    return q
+
+
+def signal_band_quadform_fast(grid: SamplingGrid, band: SignalBand, w, device: int = 0):
+    """The same w^T R(B) w in O(N log N): windowed lattice sum of |W(f)|^2 over [-F, F] from the
+    path's own type-1 NUFFT (normalise.cu)."""
+    t = C.f64(grid.times())
+    w = C.f64(np.atleast_2d(w))
+    q = np.empty(w.shape[0])
+    C.check(C.lib().nus_signal_band_quadform_fast(C.dptr(t), t.size, band.f_max, C.dptr(w), w.shape[0],
+                                                  device, C.dptr(q)))
     return q
 
 

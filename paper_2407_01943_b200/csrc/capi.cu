@@ -410,6 +410,20 @@ int nus_signal_band_quadform(const double* times, int64_t n, double f_max, const
   });
 }
 
+int nus_signal_band_quadform_fast(const double* times, int64_t n, double f_max, const double* w_host,
+                                  int64_t k, int32_t device, double* q_host) {
+  return guarded([&] {
+    nus::require(times && w_host && q_host, "quadratic_form: null argument");
+    nus::require(n >= 2, "SamplingGrid: need at least 2 samples");
+    nus::require(f_max > 0.0 && std::isfinite(f_max), "SignalBand: f_max must be positive");
+    nus::use_device(device);
+    nus::DeviceBuffer t(n * sizeof(double)), w(static_cast<size_t>(k) * n * sizeof(double));
+    NUS_CUDA(cudaMemcpy(t.ptr, times, t.bytes, cudaMemcpyHostToDevice));
+    NUS_CUDA(cudaMemcpy(w.ptr, w_host, w.bytes, cudaMemcpyHostToDevice));
+    nus::quadform_fast_device(t.as<double>(), times, n, f_max, w.as<double>(), k, q_host, 0, device);
+  });
+}
+
 int nus_taper_spline(const double* times, int64_t n, double f_max, double f_w, int64_t k,
                      int32_t device, double* w_host) {
   return guarded([&] {

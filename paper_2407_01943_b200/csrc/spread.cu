@@ -678,6 +678,9 @@ void spread_typed(const Plan& plan, const SpreadArgs& a, cudaStream_t s) {
     return !(e && std::strcmp(e, "gather") == 0);
   }();
   require(use_tc || p.kernel == NUS_KERNEL_GAUSSIAN, "spread: the gather kernel implements the Gaussian only");
+  // the tensor-core kernel's weight rows hold one 32-cell window: wider Gaussians (eps < ~2e-13,
+  // 2w > 32) take the gather kernel; the ES window is at most 16 cells
+  const bool tc = use_tc && p.sw <= 32;
   const int ns = p.kernel == NUS_KERNEL_ES ? p.sw : 0;
   // taper groups of at most 8, balanced
   const int64_t k = a.tapers ? a.k : 1;
@@ -687,7 +690,7 @@ void spread_typed(const Plan& plan, const SpreadArgs& a, cudaStream_t s) {
     const int64_t kg = (k - k0 + (groups - gidx) - 1) / (groups - gidx);
     P.k0 = static_cast<int>(k0);
     P.kg = static_cast<int>(kg);
-    if (use_tc) {
+    if (tc) {
       launch_tc_x<Real>(P, ns, s);
       k0 += kg;
       continue;

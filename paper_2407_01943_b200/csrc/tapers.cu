@@ -17,6 +17,8 @@
 #include <cfloat>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 
 #include "nus_internal.cuh"
 
@@ -1081,6 +1083,15 @@ __global__ void scale_by_kernel(double* __restrict__ w, int64_t n, int k, const 
 }
 }  // namespace
 
+bool normalise_exact(int64_t n) {
+  const char* e = std::getenv("NUS_NORMALISE");
+  if (e && std::strcmp(e, "exact") == 0) return true;
+  if (e && std::strcmp(e, "fast") == 0) return false;
+  const char* m = std::getenv("NUS_QUADFORM_EXACT_MAX");
+  const int64_t lim = m ? std::atoll(m) : (int64_t{1} << 18);
+  return n <= lim;
+}
+
 void gpss_interpolated_device(const double* d_t, const double* h_t, int64_t n, double f_max,
                               double f_w, int64_t k, double* d_w, cudaStream_t s, double* ms_dpss,
                               double* ms_spline, double* ms_norm) {
@@ -1103,9 +1114,15 @@ void gpss_interpolated_device(const double* d_t, const double* h_t, int64_t n, d
   if (ms_spline) *ms_spline = host_ms_since(t0);
   t0 = std::chrono::steady_clock::now();
   std::vector<double> q(k), scale(k);
-  for (int64_t k0 = 0; k0 < k; k0 += kQfGroup) {
-    const int64_t kk = std::min<int64_t>(kQfGroup, k - k0);
-    quadform_device(d_t, n, f_max, d_w + k0 * n, kk, 0, n, q.data() + k0, s);
+  if (normalise_exact(n)) {
+    for (int64_t k0 = 0; k0 < k; k0 += kQfGroup) {
+      const int64_t kk = std::min<int64_t>(kQfGroup, k - k0);
+      quadform_device(d_t, n, f_max, d_w + k0 * n, kk, 0, n, q.data() + k0, s);
+    }
+  } else {  // O(N log N) lattice form of the same quadratic form (normalise.cu)
+    int dev = 0;
+    NUS_CUDA(cudaGetDevice(&dev));
+    quadform_fast_device(d_t, h_t, n, f_max, d_w, k, q.data(), s, dev);
   }
   for (int64_t j = 0; j < k; ++j) {
     if (!(q[j] > 0.0)) fail(NUS_ERR_NUMERIC, "gpss_interpolated: degenerate metric norm");
