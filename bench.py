@@ -59,8 +59,9 @@ def make_workload(name, rank):
         return W.c3(channels=int(os.environ.get("NUS_C3_CHANNELS", "32")), first_channel=32 * rank)
     if name == "c5":
         return W.c5()
-    if name == "c4":
-        return W.c4()
+    if name == "c4":  # C4's structure; N defaults to 2^22 (DPSS setup at 2^26)
+        lg = int(os.environ.get("NUS_C4_LOG2N", "22"))
+        return W.c4(n=1 << lg, n_centers=1 << (lg - 2))
     if name == "c1":
         return W.c1()
     raise SystemExit(f"unknown workload {name}")
@@ -74,7 +75,7 @@ def describe(wl, name):
         "c3": f"c3: {wl.channels} channels x N=2^{int(np.log2(n))}, I=2^{int(np.log2(i))}, K={wl.k}, eps={wl.eps:g}, fp32",
         "c5": f"c5: jittered N=2^{int(np.log2(n))}, I=2^{int(np.log2(i))}, K={wl.k}, eps={wl.eps:g}, {wl.precision}",
         "c1": f"c1: N={n}, I={i}, K={wl.k}, eps={wl.eps:g}",
-        "c4": f"c4: clustered N=2^{int(np.log2(n))} (400 windows), I=2^{int(np.log2(i))}, K={wl.k} (NW={wl.nw:g}), eps={wl.eps:g}, {wl.precision}, all samples on one GPU",
+        "c4": f"c4: clustered N=2^{int(np.log2(n))} (400 windows), I=2^{int(np.log2(i))}, K={wl.k} (NW={wl.nw:g}), eps={wl.eps:g}, {wl.precision}, all samples on one GPU (BASELINE C4 is N=2^26, I=2^24)",
     }[name]
     return desc
 

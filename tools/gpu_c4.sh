@@ -1,2 +1,4 @@
-timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_all.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_all.log
-NUS_DPSS_PROF=1 timeout 900 python bench.py --workload c4 --steps 10 --warmup 3 --e2e-steps 3 --no-cpu > gpurun_out/bench_c4.log 2>&1
+timeout 900 python -m pytest tests -m gpu -q -x -k "c4 or normalisation" > gpurun_out/pytest_c4.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_c4.log
+timeout 900 python bench.py --workload c4 --steps 20 --warmup 3 --e2e-steps 5 --no-cpu > gpurun_out/bench_c4.log 2>&1
+timeout 600 python bench.py --workload c5 --steps 20 --warmup 3 --e2e-steps 5 --no-cpu > gpurun_out/bench_c5.log 2>&1
+NUS_C3_CHANNELS=32 timeout 600 python bench.py --workload c3 --steps 20 --warmup 3 --e2e-steps 5 --no-cpu > gpurun_out/bench_c3.log 2>&1
