@@ -704,12 +704,13 @@ int ilog2(int64_t v) {
 
 }  // namespace
 
-bool pdl_enabled() {  // opt-in: measured slower on C2 (0.312 vs 0.283 ms per spectrum)
-  static const bool on = [] {
-    const char* e = std::getenv("NUS_PDL");
-    return e && std::strcmp(e, "1") == 0;
-  }();
-  return on;
+bool pdl_enabled() {
+  // Programmatic dependent launch stays off.  Measured on C2 (ES window): 0.288 ms per spectrum
+  // with it against 0.264 without, also with last-wave-only triggers and with the spread not
+  // waiting on pass B.  It is also unsafe here: a programmatic launch overlapped a preceding
+  // H2D copy on the same stream (the host estimate read the previous x), so the launch attribute
+  // is never set; the griddepcontrol instructions in the kernels are then no-ops.
+  return false;
 }
 
 bool fused_fft_supported(const PlanParams& p) {

@@ -254,9 +254,9 @@ __host__ __device__ inline int64_t imin64(int64_t a, int64_t b) { return a < b ?
 // ---- programmatic dependent launch ---------------------------------------------------
 // The per-spectrum kernels are launched with programmatic stream serialisation: a kernel's
 // CTAs may be dispatched while its predecessor drains, and each waits (griddepcontrol.wait:
-// predecessor complete, memory visible) before its first dependent read, so stream order is
-// unchanged; only launch latency and the predecessor's tail are overlapped.  Opt-in
-// (NUS_PDL=1): on C2 the early-dispatched CTAs held slots and the step got slower.
+// predecessor complete, memory visible) before its first dependent read.  Disabled (see
+// pdl_enabled in fft.cu): slower on C2, and a programmatic launch was seen to overlap an H2D
+// copy queued before it on the same stream.
 bool pdl_enabled();
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
