@@ -296,6 +296,50 @@ __global__ void __launch_bounds__(32) inverse_iteration_dd_warp_kernel(
   }
 }
 
+// x_j <- x_j * scale_j in double-double (normalised start vectors for a refined second run)
+__global__ void dd_scale_kernel(dd* __restrict__ xs, const double* __restrict__ scales, int64_t n, int k) {
+  const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (g >= n * k) return;
+  const int64_t j = g / n;
+  xs[g] = dd_mul(xs[g], dd{scales[2 * j], scales[2 * j + 1]});
+}
+
+// Rayleigh-quotient correction of the shift: per block, sum x_i r_i and x_i^2 with
+// r = (T - sigma) x formed in double-double (|T| ~ N^2 / 4 against a residual of O(gap) |x|:
+// the cancellation needs the extra precision; the sums themselves do not)
+constexpr int kRqThreads = 256;
+__global__ void __launch_bounds__(kRqThreads) rayleigh_partials_kernel(
+    const double* __restrict__ d, const double* __restrict__ e, int64_t n, const dd* __restrict__ xs,
+    const double* __restrict__ sigma_hi, const double* __restrict__ sigma_lo, double* __restrict__ partial) {
+  const int j = blockIdx.y;
+  const dd* x = xs + static_cast<int64_t>(j) * n;
+  const dd sig = {sigma_hi[j], sigma_lo[j]};
+  double xr = 0.0, xx = 0.0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(kRqThreads) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * kRqThreads) {
+    dd r = dd_mul(dd_sub(dd_from(d[i]), sig), x[i]);
+    if (i > 0) r = dd_add(r, dd_mul_d(x[i - 1], e[i - 1]));
+    if (i + 1 < n) r = dd_add(r, dd_mul_d(x[i + 1], e[i]));
+    xr += x[i].hi * r.hi;
+    xx += x[i].hi * x[i].hi;
+  }
+  __shared__ double s0[kRqThreads], s1[kRqThreads];
+  s0[threadIdx.x] = xr;
+  s1[threadIdx.x] = xx;
+  __syncthreads();
+  for (int o = kRqThreads / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      s0[threadIdx.x] += s0[threadIdx.x + o];
+      s1[threadIdx.x] += s1[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    partial[2 * (static_cast<int64_t>(j) * gridDim.x + blockIdx.x)] = s0[0];
+    partial[2 * (static_cast<int64_t>(j) * gridDim.x + blockIdx.x) + 1] = s1[0];
+  }
+}
+
 // out[j][i] = x_j[i] * scale_j  (dd -> fp64)
 __global__ void dd_finalize_kernel(const dd* __restrict__ xs, const double* __restrict__ scales,
                                    int64_t n, int k, double* __restrict__ out) {
@@ -816,7 +860,12 @@ DpssResult tridiag_top_device(const double* d_diag, const double* d_off, int64_t
   DeviceBuffer d_lo(k * sizeof(double)), d_hi(k * sizeof(double)), d_cnt(k * probes * sizeof(int32_t));
   std::vector<int32_t> cnt(k * probes);
   const double pivmin = anorm * DBL_EPSILON * 1e-3;
-  const double target = 16.0 * DBL_EPSILON * anorm;
+  // Large n (the DPSS matrix has ||T|| ~ n^2/2 but eigenvalue gaps of O(10) for every n, e.g.
+  // 12.75 .. 24.6 at NW = 8): bisect to 2 eps ||T|| and refine every shift by a double-double
+  // Rayleigh quotient (below), since at n = 2^26 16 eps ||T|| would exceed half a gap.
+  const char* force_refine = std::getenv("NUS_DPSS_REFINE");
+  const bool refine = n >= (int64_t{1} << 21) || (force_refine && force_refine[0] == '1');
+  const double target = (refine ? 2.0 : 16.0) * DBL_EPSILON * anorm;
   for (int pass = 0; pass < 16; ++pass) {
     bool done = true;
     for (int64_t j = 0; j < k; ++j) done = done && (hi[j] - lo[j] <= target);
@@ -883,6 +932,41 @@ DpssResult tridiag_top_device(const double* d_diag, const double* d_off, int64_t
   note_launch();
   check_launch("inverse_iteration_dd_warp_kernel");
   lap("inverse iteration");
+  if (refine) {  // shift <- shift + x^T (T - shift) x / x^T x, then two more iterations
+    dd_scale_kernel<<<blocks_for(n * k, 256), 256, 0, s>>>(xs.as<dd>(), d_norm.as<double>(), n, static_cast<int>(k));
+    note_launch();
+    const unsigned rb = 296;
+    DeviceBuffer part(static_cast<size_t>(k) * rb * 2 * sizeof(double));
+    rayleigh_partials_kernel<<<dim3(rb, static_cast<unsigned>(k)), kRqThreads, 0, s>>>(
+        d_diag, d_off, n, xs.as<dd>(), d_sh.as<double>(), d_sl.as<double>(), part.as<double>());
+    note_launch();
+    check_launch("rayleigh_partials_kernel");
+    std::vector<double> hp(static_cast<size_t>(k) * rb * 2);
+    NUS_CUDA(cudaMemcpyAsync(hp.data(), part.ptr, hp.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+    NUS_CUDA(cudaStreamSynchronize(s));
+    for (int64_t j = 0; j < k; ++j) {
+      long double xr = 0.0L, xx = 0.0L;
+      for (unsigned b = 0; b < rb; ++b) {
+        xr += hp[2 * (j * rb + b)];
+        xx += hp[2 * (j * rb + b) + 1];
+      }
+      const double mu = static_cast<double>(xr / xx);
+      // (sig_hi + sig_lo) + mu as a normalised double-double
+      const double s1 = sig_hi[j] + mu, bb = s1 - sig_hi[j];
+      const double err = (sig_hi[j] - (s1 - bb)) + (mu - bb) + sig_lo[j];
+      sig_hi[j] = s1 + err;
+      sig_lo[j] = err - (sig_hi[j] - s1);
+      res.values[j] = sig_hi[j];
+    }
+    NUS_CUDA(cudaMemcpyAsync(d_sh.ptr, sig_hi.data(), k * sizeof(double), cudaMemcpyHostToDevice, s));
+    NUS_CUDA(cudaMemcpyAsync(d_sl.ptr, sig_lo.data(), k * sizeof(double), cudaMemcpyHostToDevice, s));
+    inverse_iteration_dd_warp_kernel<<<static_cast<unsigned>(k), 32, 0, s>>>(
+        d_diag, d_off, n, d_sh.as<double>(), d_sl.as<double>(), 2, pivmin, xs.as<dd>(), us.as<dd>(),
+        d_norm.as<double>());
+    note_launch();
+    check_launch("inverse_iteration_dd_warp_kernel (refined)");
+    lap("rayleigh refinement + 2 iterations");
+  }
   dd_finalize_kernel<<<blocks_for(n * k, 256), 256, 0, s>>>(xs.as<dd>(), d_norm.as<double>(), n,
                                                             static_cast<int>(k), d_vec);
   note_launch();
@@ -890,7 +974,7 @@ DpssResult tridiag_top_device(const double* d_diag, const double* d_off, int64_t
     // (near-)degenerate eigenvalues, which no inverse iteration separates: the reference's
     // start-vector / re-orthogonalisation rule.  Pairs the double-double iteration resolves
     // (DPSS gaps are ~1e-8 ||T|| at N = 2^16) keep the fast path: their eigenvectors are unique.
-    const double cluster_tol = anorm * 1e-13;
+    const double cluster_tol = refine ? 8.0 * DBL_EPSILON * anorm : anorm * 1e-13;
     std::vector<int32_t> offs{0}, members, starts;
     std::vector<double> lam, lam_solve;
     std::vector<char> used(n, 0);

@@ -152,3 +152,16 @@ def test_fast_normalisation_matches_exact_quadform(cfg):
     qe = nus.signal_band_quadform(g, band, w)
     qf = nus.signal_band_quadform_fast(g, band, w)
     assert np.abs(qf / qe - 1).max() < 1e-10
+
+
+@pytest.mark.parametrize("n,tw,k,force", [(1 << 16, 8.0, 15, True), (1 << 18, 8.0, 15, True), (1 << 21, 8.0, 15, False)])
+def test_dpss_rayleigh_refined_vs_extended_precision_oracle(n, tw, k, force, monkeypatch):
+    """Large-n DPSS path (n >= 2^21, or NUS_DPSS_REFINE=1): bisection to 2 eps ||T||, double-double
+    inverse iteration, a double-double Rayleigh-quotient shift and two more iterations; the gaps of
+    the commuting tridiagonal stay O(10) while ||T|| ~ n^2/2, the regime of C4 (NW=8, K=15)."""
+    if force:
+        monkeypatch.setenv("NUS_DPSS_REFINE", "1")
+    d = nus.dpss_uniform(n, tw, k, concentrations=False)
+    tc, ev = C.dpss(n, tw, k)
+    assert np.abs(sign_align(d.tapers, tc) - tc).max() < 1e-10
+    np.testing.assert_allclose(d.eigenvalues, ev, rtol=1e-13)
