@@ -320,20 +320,20 @@ __device__ inline void tc_advance(TcCursor& u, int4& pre, TcPos& pp, const Sprea
 }
 
 // x kinds (template XK): 0 f64 real, 1 f64 complex, 2 f32 real, 3 f32 complex
-template <typename Real>
+template <typename Real, int G>
 struct TcPoint {  // this lane's prefetched point of the next round: raw loads only, so the
                   // loads stay in flight until the round is staged
   int start, ti;
   unsigned long long xa, xb;  // x bits (f64 re/im, or f32 pair / scalar in xa)
   typename Vec2<Real>::T ph, ag;
-  Real w[8];
+  Real w[8 * G];
 };
 
 // Every load is unconditional (clamped point index, clamped taper row): lanes past the
 // round's points read a real point with ti = -1, which the staging masks to x = 0; rows
 // k >= kg are read but never staged.  No lane-divergent branch, no use of loaded values.
-template <typename Real, int XK>
-__device__ inline void tc_load(TcPoint<Real>& q, int ti, const TcCursor& u, int lane, const SpreadParams<Real>& P) {
+template <typename Real, int XK, int G>
+__device__ inline void tc_load(TcPoint<Real, G>& q, int ti, const TcCursor& u, int lane, const SpreadParams<Real>& P) {
   using R2 = typename Vec2<Real>::T;
   if (!u.valid || u.nb == 0) return;  // warp-uniform
   const bool has = lane < u.nb;
@@ -357,7 +357,7 @@ __device__ inline void tc_load(TcPoint<Real>& q, int ti, const TcCursor& u, int 
   const Real* tp =
       P.taper_base + (static_cast<int64_t>(u.c) * P.k_total + P.k0) * P.tstride_k + (u.b0 + j) * P.tstride_j;
 #pragma unroll
-  for (int k = 0; k < 8; ++k) q.w[k] = tp[min(k, P.kg - 1) * P.tstride_k];
+  for (int k = 0; k < 8 * G; ++k) q.w[k] = tp[min(k, P.kg - 1) * P.tstride_k];
 }
 
 template <typename Real>
@@ -371,17 +371,19 @@ __constant__ double c_es[kEsTableSize];
 
 // NS = 0: the reference's Gaussian (support P.w2, geometric chains); NS > 0: the ES window on NS
 // cells, weight of cell p = Horner(c_es[ns block][p], 2 fr - 1).
-template <typename Real, int XK, int NS>
-__global__ void __launch_bounds__(kTcWarps * 32, kTcCtasPerSm) spread_tc_kernel(const SpreadParams<Real> P) {
+// G taper groups of 8 share one staging of the points (K = 9..16 with G = 2: Z rows 8 G,
+// accumulators per group; 3 CTAs / SM instead of 5)
+template <typename Real, int XK, int NS, int G = 1>
+__global__ void __launch_bounds__(kTcWarps * 32, G == 1 ? kTcCtasPerSm : 3) spread_tc_kernel(const SpreadParams<Real> P) {
   using R2 = typename Vec2<Real>::T;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int RS = kTcRows;
-  constexpr size_t kWarpBytes = (8 * RS) * sizeof(double2) + (kTcPts * RS) * sizeof(double) + RS * sizeof(int);
+  constexpr size_t kWarpBytes = (8 * G * RS) * sizeof(double2) + (kTcPts * RS) * sizeof(double) + RS * sizeof(int);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   double* scq = reinterpret_cast<double*>(smem_raw);     // C_p
   unsigned char* mine = smem_raw + kMaxW2 * sizeof(double) + warp * kWarpBytes;
   double2* sz = reinterpret_cast<double2*>(mine);        // Z [8 tapers][RS points] (rows >= KG stay 0)
-  double* sw = reinterpret_cast<double*>(sz + 8 * RS);   // W [kTcPts points][RS], slot = cell mod 32
+  double* sw = reinterpret_cast<double*>(sz + 8 * G * RS);  // W [kTcPts points][RS], slot = cell mod 32
   int* srel = reinterpret_cast<int*>(sw + kTcPts * RS);  // rel [RS points]
 
   const int w2 = NS > 0 ? NS : P.w2;
@@ -406,14 +408,16 @@ __global__ void __launch_bounds__(kTcWarps * 32, kTcCtasPerSm) spread_tc_kernel(
   tc_advance(n1, pre, pp, P, stride);
   n2 = n1;
   tc_advance(n2, pre, pp, P, stride);
-  TcPoint<Real> pt;
+  TcPoint<Real, G> pt;
   pt.ti = -1;
-  tc_load<Real, XK>(pt, tc_perm(cur, lane, P), cur, lane, P);
+  tc_load<Real, XK, G>(pt, tc_perm(cur, lane, P), cur, lane, P);
   int perm_next = tc_perm(n1, lane, P);
 
-  double cr[4][2], ci[4][2];
+  double cr[G][4][2], ci[G][4][2];
 #pragma unroll
-  for (int b = 0; b < 4; ++b) cr[b][0] = cr[b][1] = ci[b][0] = ci[b][1] = 0.0;
+  for (int gg = 0; gg < G; ++gg)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) cr[gg][b][0] = cr[gg][b][1] = ci[gg][b][0] = ci[gg][b][1] = 0.0;
 
   const int64_t off_h0 = static_cast<int64_t>(2 * t) * P.mr, off_h1 = off_h0 + P.mr;  // tapers 2t, 2t+1
   while (cur.valid) {
@@ -438,7 +442,7 @@ __global__ void __launch_bounds__(kTcWarps * 32, kTcCtasPerSm) spread_tc_kernel(
       const double pr = static_cast<double>(pt.ph.x), pi = static_cast<double>(pt.ph.y);
       const double yr = xr * pr - xi * pi, yi = xr * pi + xi * pr;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {  // rows k >= kg are never written: they stay zero
+      for (int k = 0; k < 8 * G; ++k) {  // rows k >= kg are never written: they stay zero
         const double wk = static_cast<double>(pt.w[k]);
         if (k < P.kg) sz[k * RS + lane] = double2{wk * yr, wk * yi};
       }
@@ -473,7 +477,7 @@ __global__ void __launch_bounds__(kTcWarps * 32, kTcCtasPerSm) spread_tc_kernel(
     }
     __syncwarp();
     // ---- prefetch round n1 (its perm is in hand) and the perm of round n2
-    tc_load<Real, XK>(pt, perm_next, n1, lane, P);
+    tc_load<Real, XK, G>(pt, perm_next, n1, lane, P);
     perm_next = tc_perm(n2, lane, P);
     // ---- per block: its point range by ballot (rel ascends over the lanes), then exact
     // 4-point steps on the tensor cores; a = W(cell - rel) masked to the support
@@ -488,23 +492,29 @@ __global__ void __launch_bounds__(kTcWarps * 32, kTcCtasPerSm) spread_tc_kernel(
         const int pp = 8 * b + g - rcol[p0];
         const double wv = wrow[p0 * RS + 8 * b];
         const double a = static_cast<unsigned>(pp) < static_cast<unsigned>(w2) ? wv : 0.0;
-        const double2 zb = zcol[p0];
-        dmma_8x8x4(cr[b][0], cr[b][1], a, zb.x);
-        dmma_8x8x4(ci[b][0], ci[b][1], a, zb.y);
+#pragma unroll
+        for (int gg = 0; gg < G; ++gg) {  // taper group gg: Z rows 8 gg .. 8 gg + 7
+          const double2 zb = zcol[gg * 8 * RS + p0];
+          dmma_8x8x4(cr[gg][b][0], cr[gg][b][1], a, zb.x);
+          dmma_8x8x4(ci[gg][b][0], ci[gg][b][1], a, zb.y);
+        }
       }
     }
     if (cur.last) {
       R2* out = P.grid + (static_cast<int64_t>(cur.c) * P.kpad + P.k0) * P.mr;
-      R2* out0 = out + off_h0;
-      R2* out1 = out + off_h1;
-      const bool k0ok = 2 * t < P.kg, k1ok = 2 * t + 1 < P.kg;
       const int cell0 = static_cast<int>(cur.seg) * 32 + g;
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int addr = cell_addr32(cell0 + 8 * b, P.blocked, P.lgC, P.lgCW, P.lgT);
-        if (k0ok) out0[addr] = R2{static_cast<Real>(cr[b][0]), static_cast<Real>(ci[b][0])};
-        if (k1ok) out1[addr] = R2{static_cast<Real>(cr[b][1]), static_cast<Real>(ci[b][1])};
-        cr[b][0] = cr[b][1] = ci[b][0] = ci[b][1] = 0.0;
+      for (int gg = 0; gg < G; ++gg) {
+        R2* out0 = out + off_h0 + static_cast<int64_t>(8 * gg) * P.mr;
+        R2* out1 = out + off_h1 + static_cast<int64_t>(8 * gg) * P.mr;
+        const bool k0ok = 8 * gg + 2 * t < P.kg, k1ok = 8 * gg + 2 * t + 1 < P.kg;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int addr = cell_addr32(cell0 + 8 * b, P.blocked, P.lgC, P.lgCW, P.lgT);
+          if (k0ok) out0[addr] = R2{static_cast<Real>(cr[gg][b][0]), static_cast<Real>(ci[gg][b][0])};
+          if (k1ok) out1[addr] = R2{static_cast<Real>(cr[gg][b][1]), static_cast<Real>(ci[gg][b][1])};
+          cr[gg][b][0] = cr[gg][b][1] = ci[gg][b][0] = ci[gg][b][1] = 0.0;
+        }
       }
     }
     __syncwarp();  // private tables are restaged next
@@ -527,26 +537,26 @@ void es_upload() {  // once per device
   if (dev < 64) done[dev] = true;
 }
 
-template <typename Real, int XK, int NS>
+template <typename Real, int XK, int NS, int G = 1>
 void launch_tc(const SpreadParams<Real>& P, cudaStream_t s) {
   const size_t warp_bytes =
-      (8 * kTcRows) * sizeof(double2) + (kTcPts * kTcRows) * sizeof(double) + kTcRows * sizeof(int);
+      (8 * G * kTcRows) * sizeof(double2) + (kTcPts * kTcRows) * sizeof(double) + kTcRows * sizeof(int);
   const size_t smem = kMaxW2 * sizeof(double) + kTcWarps * warp_bytes;
   static int blocks_per_sm = 0, sms = 0;
   if (blocks_per_sm == 0) {
-    NUS_CUDA(cudaFuncSetAttribute(spread_tc_kernel<Real, XK, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    NUS_CUDA(cudaFuncSetAttribute(spread_tc_kernel<Real, XK, NS, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
     int dev = 0;
     NUS_CUDA(cudaGetDevice(&dev));
     NUS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    NUS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, spread_tc_kernel<Real, XK, NS>,
+    NUS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, spread_tc_kernel<Real, XK, NS, G>,
                                                            kTcWarps * 32, smem));
     require(blocks_per_sm > 0, "spread: tensor-core kernel does not fit on an SM");
   }
   const int64_t warps = P.nseg_used * P.channels;
   const int64_t grid = std::min<int64_t>((warps + kTcWarps - 1) / kTcWarps, static_cast<int64_t>(blocks_per_sm) * sms);
   if constexpr (NS > 0) es_upload();
-  launch_pdl(spread_tc_kernel<Real, XK, NS>, dim3(static_cast<unsigned>(grid)), dim3(kTcWarps * 32), smem, s, P);
+  launch_pdl(spread_tc_kernel<Real, XK, NS, G>, dim3(static_cast<unsigned>(grid)), dim3(kTcWarps * 32), smem, s, P);
   note_launch();
   check_launch("spread_tc_kernel");
 }
@@ -554,23 +564,23 @@ void launch_tc(const SpreadParams<Real>& P, cudaStream_t s) {
 __device__ double g_one_f64 = 1.0;
 __device__ float g_one_f32 = 1.0f;
 
-template <typename Real, int XK>
+template <typename Real, int XK, int G = 1>
 void launch_tc_ns(const SpreadParams<Real>& P, int ns, cudaStream_t s) {
   switch (ns) {
-    case 0: launch_tc<Real, XK, 0>(P, s); break;
-    case 4: launch_tc<Real, XK, 4>(P, s); break;
-    case 6: launch_tc<Real, XK, 6>(P, s); break;
-    case 8: launch_tc<Real, XK, 8>(P, s); break;
-    case 10: launch_tc<Real, XK, 10>(P, s); break;
-    case 12: launch_tc<Real, XK, 12>(P, s); break;
-    case 14: launch_tc<Real, XK, 14>(P, s); break;
-    case 16: launch_tc<Real, XK, 16>(P, s); break;
+    case 0: launch_tc<Real, XK, 0, G>(P, s); break;
+    case 4: launch_tc<Real, XK, 4, G>(P, s); break;
+    case 6: launch_tc<Real, XK, 6, G>(P, s); break;
+    case 8: launch_tc<Real, XK, 8, G>(P, s); break;
+    case 10: launch_tc<Real, XK, 10, G>(P, s); break;
+    case 12: launch_tc<Real, XK, 12, G>(P, s); break;
+    case 14: launch_tc<Real, XK, 14, G>(P, s); break;
+    case 16: launch_tc<Real, XK, 16, G>(P, s); break;
     default: fail(NUS_ERR_INVALID_ARGUMENT, "spread: unsupported ES width");
   }
 }
 
 template <typename Real>
-void launch_tc_x(SpreadParams<Real> P, int ns, cudaStream_t s) {
+void launch_tc_x(SpreadParams<Real> P, int ns, cudaStream_t s, bool two_groups = false) {
   if (P.tapers) {
     P.taper_base = P.tapers;
     P.tstride_k = P.n;
@@ -584,6 +594,12 @@ void launch_tc_x(SpreadParams<Real> P, int ns, cudaStream_t s) {
     P.tstride_j = 0;
   }
   const int xk = P.x_dtype == 0 ? (P.x_complex ? 1 : 0) : (P.x_complex ? 3 : 2);
+  if (two_groups) {  // real x only (the estimator's spectra)
+    require(xk == 0 || xk == 2, "spread: two taper groups need real x");
+    if (xk == 0) launch_tc_ns<Real, 0, 2>(P, ns, s);
+    else launch_tc_ns<Real, 2, 2>(P, ns, s);
+    return;
+  }
   switch (xk) {
     case 0: launch_tc_ns<Real, 0>(P, ns, s); break;
     case 1: launch_tc_ns<Real, 1>(P, ns, s); break;
@@ -682,8 +698,19 @@ void spread_typed(const Plan& plan, const SpreadArgs& a, cudaStream_t s) {
   // 2w > 32) take the gather kernel; the ES window is at most 16 cells
   const bool tc = use_tc && p.sw <= 32;
   const int ns = p.kernel == NUS_KERNEL_ES ? p.sw : 0;
-  // taper groups of at most 8, balanced
   const int64_t k = a.tapers ? a.k : 1;
+  // 9..16 tapers of a real series: both groups from one staging of the points
+  static const bool two_ok = [] {
+    const char* e = std::getenv("NUS_SPREAD_GROUPS");
+    return !(e && std::strcmp(e, "1") == 0);
+  }();
+  if (tc && two_ok && k > 8 && k <= 16 && !a.x_complex) {
+    P.k0 = 0;
+    P.kg = static_cast<int>(k);
+    launch_tc_x<Real>(P, ns, s, true);
+    return;
+  }
+  // taper groups of at most 8, balanced
   const int64_t groups = (k + 7) / 8;
   int64_t k0 = 0;
   for (int64_t gidx = 0; gidx < groups; ++gidx) {
