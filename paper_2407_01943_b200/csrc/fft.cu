@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(kFftThreads, 2) fft_cols_kernel(
 // NT * 16 elements) per CTA, several CTAs per SM in flight instead of a persistent bulk-copy
 // pipeline.  Rows outside the occupied interval are zeros and are not read.
 template <typename Real, int R0, int NT>
-__global__ void __launch_bounds__(NT, NT == 128 ? 4 : 2) fft_cols_blk_kernel(
+__global__ void __launch_bounds__(NT, NT == 128 ? 4 : NT == 256 ? 2 : 1) fft_cols_blk_kernel(
     const typename C2<Real>::T* __restrict__ grid, typename C2<Real>::T* __restrict__ out, int64_t mr, int R, int C,
     int CW, int k, int kpad, const typename C2<Real>::T* __restrict__ tw_r,
     const typename C2<Real>::T* __restrict__ tw_hi, const typename C2<Real>::T* __restrict__ tw_lo, int lo_bits,
@@ -322,7 +322,7 @@ __host__ __device__ constexpr int crop_q(int c) { return c < 5 ? c : c + 7; }
 // NT threads per row: 256 for C = 4096 (2 CTAs / SM), 128 for C = 2048 (4 CTAs / SM, twice the
 // rows in flight to cover the row loads).
 template <typename Real, typename PReal, int R0, int NT = kFftThreads>
-__global__ void __launch_bounds__(NT, NT == 128 ? 4 : 2) fft_rows_crop_kernel(
+__global__ void __launch_bounds__(NT, NT == 128 ? 4 : NT == 256 ? 2 : 1) fft_rows_crop_kernel(
     const typename C2<Real>::T* __restrict__ grid, int64_t mr, int R, int C, int RPC, int64_t kpad,
     int k_count, int64_t nc, int64_t mode_offset, const Real* __restrict__ deconv,
     const typename C2<Real>::T* __restrict__ tw_c, typename C2<Real>::T* __restrict__ j_out,
@@ -715,7 +715,8 @@ bool pdl_enabled() {
 
 bool fused_fft_supported(const PlanParams& p) {
   // 4096-element in-CTA FFTs need >= 2 stages per pass: C = 4096 rows, R = Mr / 4096 = 1 or >= 32
-  return p.mr == kFftElems || (p.mr >= (int64_t{1} << 17) && p.mr <= (int64_t{1} << 24));
+  // Mr = 2^25 (C4) runs both passes as 8192-element in-CTA FFTs (512 threads, 128 KB tiles)
+  return p.mr == kFftElems || (p.mr >= (int64_t{1} << 17) && p.mr <= (int64_t{1} << 25));
 }
 
 void fused_fft_prepare(Plan& plan) {
@@ -733,6 +734,8 @@ void fused_fft_prepare(Plan& plan) {
     const bool c4096 = e && std::strcmp(e, "4096") == 0;
     f.C = (!c4096 && p.mr >= (int64_t{1} << 17) && p.mr <= (int64_t{1} << 23)) ? kFftElems / 2 : kFftElems;
   }
+  const bool wide = p.mr == (int64_t{1} << 25);  // 8192-element tiles and rows
+  if (wide) f.C = 2 * kFftElems;
   f.R = static_cast<int>(p.mr / f.C);
   f.RPC = 1;
   {  // pass A: register-loading 4096-cell tiles (default; 96.4 vs 107.4 us for the bulk-copy
@@ -741,7 +744,8 @@ void fused_fft_prepare(Plan& plan) {
     f.cols_mode = (e && std::strcmp(e, "async") == 0) ? 2 : (e && std::strcmp(e, "reg128") == 0) ? 0 : 1;
   }
   if (f.cols_mode == 0 && f.R > kFftElems / 2) f.cols_mode = 1;  // a 2048-cell tile must hold >= 1 column
-  const int tile = f.cols_mode == 0 ? kFftElems / 2 : kFftElems;
+  if (wide) f.cols_mode = 3;  // R = 4096 rows x CW = 2 columns per 8192-cell tile
+  const int tile = f.cols_mode == 0 ? kFftElems / 2 : f.cols_mode == 3 ? 2 * kFftElems : kFftElems;
   f.CW = f.R > 1 ? tile / f.R : 0;
   f.lo_bits = lg / 2;
   // blocked grid layout + bulk-copy (asynchronous) passes unless NUS_FFT_ASYNC=0
@@ -789,6 +793,14 @@ void fused_fft_prepare(Plan& plan) {
     NUS_ATTR((fft_cols_blk_kernel<double, 4, kFftThreads>));
     NUS_ATTR((fft_cols_blk_kernel<double, 2, kFftThreads>));
 #undef NUS_ATTR
+    const int smem_w = 2 * kFftElems * static_cast<int>(sizeof(double2));
+#define NUS_ATTRW(KERN) NUS_CUDA(cudaFuncSetAttribute(KERN, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_w))
+    NUS_ATTRW((fft_cols_blk_kernel<double, 16, 512>));
+    NUS_ATTRW((fft_cols_blk_kernel<float, 16, 512>));
+    NUS_ATTRW((fft_rows_crop_kernel<double, double, 2, 512>));
+    NUS_ATTRW((fft_rows_crop_kernel<float, float, 2, 512>));
+    NUS_ATTRW((fft_rows_crop_kernel<float, double, 2, 512>));
+#undef NUS_ATTRW
     const int smem2 = kBufs * kFftElems * static_cast<int>(sizeof(double2)) + kBufs * 8;
 #define NUS_ATTR2(KERN) NUS_CUDA(cudaFuncSetAttribute(KERN, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2))
     NUS_ATTR2((fft_cols_async_kernel<double, 16>));
@@ -846,7 +858,10 @@ void launch_cols(const Plan& plan, void* grid, void* scratch, int64_t k, int64_t
   launch_pdl(fft_cols_blk_kernel<Real, R0, NT>, dim3(static_cast<unsigned>(ntiles)), dim3(NT),                \
              static_cast<size_t>(NT) * 16 * sizeof(T2), s, static_cast<const T2*>(g), out, p.mr, f.R, f.C, f.CW, \
              static_cast<int>(k), static_cast<int>(kpad), tr, th, tl, f.lo_bits, f.row_lo, f.row_cnt)
-    if (f.cols_mode == 0) {
+    if (f.cols_mode == 3) {
+      require(r0 == 16, "fft: unexpected first radix for 8192-element tiles");
+      NUS_COLS_REG(16, 512);
+    } else if (f.cols_mode == 0) {
       if (r0 == 16) NUS_COLS_REG(16, 128);
       else if (r0 == 8) NUS_COLS_REG(8, 128);
       else if (r0 == 4) NUS_COLS_REG(4, 128);
@@ -915,7 +930,10 @@ void launch_rows(const Plan& plan, void* grid, int64_t k, int64_t kpad, void* j_
   launch_pdl(fft_rows_crop_kernel<Real, PReal, R0, NT>, gb, dim3(NT), smem, s, g, p.mr, f.R, f.C, 1, kpad, \
              static_cast<int>(k), p.nc, p.mode_offset, plan.tab.deconv.as<Real>(), f.tw_c.as<T2>(),       \
              static_cast<T2*>(j_out), static_cast<PReal*>(power), divisor, acc)
-  if (f.C == kFftElems / 2) {  // 2048-point rows, 128 threads
+  if (f.C == 2 * kFftElems) {  // 8192-point rows (Mr = 2^25), 512 threads
+    require(r0 == 2, "fft: unexpected first radix for 8192-point rows");
+    NUS_ROWS(2, 512);
+  } else if (f.C == kFftElems / 2) {  // 2048-point rows, 128 threads
     NUS_ROWS(8, 128);
   } else if (r0 == 16) NUS_ROWS(16, kFftThreads);
   else if (r0 == 8) NUS_ROWS(8, kFftThreads);

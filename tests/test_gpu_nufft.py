@@ -202,3 +202,21 @@ def test_clustered_dense_tiles_spill_over_batches():
     plan = nus.NufftPlan(nus.SamplingGrid(t), c, 1e-9, FAST)
     assert np.array_equal(plan.first_cells(), C.first_cells(t, c, 1e-9))
     assert rel_l2(plan.execute(y), C.nufft_fast(t, c, 1e-9, y)) < 1e-11
+
+
+@pytest.mark.parametrize("kern", ["gaussian", "es"])
+def test_fused_fft_at_mr_2_25_matches_cufft_path(kern, monkeypatch):
+    """C4's grid (I = 2^24 dyadic centres, Mr = 2^25): the fused two-pass FFT with 8192-element
+    tiles and rows agrees with the cuFFT + crop path on the same spread grid."""
+    wl = W.c4(n=1 << 18, n_centers=1 << 24, windows=100)
+    g = nus.SamplingGrid(wl.times)
+    y = wl.values.astype(np.complex128)
+    fused = nus.NufftPlan(g, wl.centers, 1e-9, FAST)
+    assert fused.grid_size() == 1 << 25
+    a = fused.execute(y)
+    monkeypatch.setenv("NUS_FFT", "cufft")
+    b = nus.NufftPlan(g, wl.centers, 1e-9, FAST).execute(y)
+    assert rel_l2(a, b) < 1e-13
+    sub = np.arange(0, 1 << 24, 4099)
+    d = C.ndft_direct(wl.times, y, wl.centers[sub])
+    assert np.abs(a[sub] - d).max() <= 1e-9 * np.abs(y).sum()
