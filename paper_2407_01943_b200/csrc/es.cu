@@ -49,7 +49,7 @@ void es_fit(int ns, double* out) {
   // Chebyshev interpolation at D + 1 Chebyshev points of s in [-1, 1] (fr = (s + 1) / 2), then
   // conversion to monomials in s; long double throughout.  Cell p of a point at cell position
   // b0 + fr (b0 = floor) is b0 - ns/2 + 1 + p, at distance u = p - ns/2 + 1 - fr.
-  const int D = ns + 1;
+  const int D = es_degree(ns);
   const long double beta = es_beta(ns);
   const long double pi = 3.141592653589793238462643383279502884L;
   std::vector<long double> s(D + 1), cheb(D + 1), mono(D + 1);

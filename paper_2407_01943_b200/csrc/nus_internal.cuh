@@ -98,13 +98,19 @@ int default_kernel();
 void set_default_kernel(int kind);
 int es_width(double eps);                 // ns: even, 4 .. 16
 inline double es_beta(int ns) { return 2.30 * ns; }
-// Monomial coefficients (in s = 2 fr - 1, degree ns + 1) of the weight of cell p = 0..ns-1 of
-// a point at fractional offset fr in [0, 1): out[p * (ns + 2) + d].
+// Degree of the window polynomials per even ns: the lowest whose max error over a cell is
+// <= ~eps_min(ns)/10 (eps_min = 10^(1-ns); the fit error plateaus at ~5% of e^-beta, the
+// square-root edge of the window)
+__host__ __device__ constexpr int es_degree(int ns) {
+  return ns <= 6 ? ns + 1 : ns == 8 ? 8 : ns <= 14 ? ns - 1 : 13;
+}
+// Monomial coefficients (in s = 2 fr - 1, degree es_degree(ns)) of the weight of cell
+// p = 0..ns-1 of a point at fractional offset fr in [0, 1): out[p * (es_degree(ns) + 1) + d].
 void es_fit(int ns, double* out);
 // Offset of ns's block in the packed table of all even ns in [kEsMinNs, kEsMaxNs].
 __host__ __device__ constexpr int es_table_offset(int ns) {
   int o = 0;
-  for (int q = kEsMinNs; q < ns; q += 2) o += q * (q + 2);
+  for (int q = kEsMinNs; q < ns; q += 2) o += q * (es_degree(q) + 1);
   return o;
 }
 constexpr int kEsTableSize = es_table_offset(kEsMaxNs + 2);

@@ -356,8 +356,13 @@ __device__ inline void tc_load(TcPoint<Real, G>& q, int ti, const TcCursor& u, i
   q.ag = P.gauss[gi];
   const Real* tp =
       P.taper_base + (static_cast<int64_t>(u.c) * P.k_total + P.k0) * P.tstride_k + (u.b0 + j) * P.tstride_j;
+  // rows k >= kg re-read row kg - 1 (never staged): the pointer stops advancing there
+  const int64_t stride = P.tstride_k;
 #pragma unroll
-  for (int k = 0; k < 8 * G; ++k) q.w[k] = tp[min(k, P.kg - 1) * P.tstride_k];
+  for (int k = 0; k < 8 * G; ++k) {
+    q.w[k] = *tp;
+    if (k + 1 < P.kg) tp += stride;
+  }
 }
 
 template <typename Real>
@@ -453,10 +458,11 @@ __global__ void __launch_bounds__(kTcWarps * 32, G == 1 ? kTcCtasPerSm : 3) spre
           double* row = sw + lane * RS;
 #pragma unroll
           for (int p = 0; p < NS; ++p) {
-            const double* cf = c_es + es_table_offset(NS) + p * (NS + 2);
-            double v = cf[NS + 1];
+            constexpr int D = es_degree(NS);
+            const double* cf = c_es + es_table_offset(NS) + p * (D + 1);
+            double v = cf[D];
 #pragma unroll
-            for (int d = NS; d >= 0; --d) v = fma(v, sv, cf[d]);
+            for (int d = D - 1; d >= 0; --d) v = fma(v, sv, cf[d]);
             row[(rel + p) & 31] = v;
           }
         }
