@@ -456,14 +456,21 @@ __global__ void __launch_bounds__(kTcWarps * 32, G == 1 ? kTcCtasPerSm : 3) spre
         if (has) {
           const double sv = 2.0 * static_cast<double>(pt.ag.x) - 1.0;
           double* row = sw + lane * RS;
+          // the window is even: cell ns-1-p at s is cell p at -s, so each pair of cells is
+          // E(s^2) +- s O(s^2) from cell p's even / odd coefficients (half the Horner steps)
+          const double s2 = sv * sv;
 #pragma unroll
-          for (int p = 0; p < NS; ++p) {
+          for (int p = 0; p < NS / 2; ++p) {
             constexpr int D = es_degree(NS);
             const double* cf = c_es + es_table_offset(NS) + p * (D + 1);
-            double v = cf[D];
+            constexpr int de = D & ~1, dod = (D - 1) | 1;  // highest even / odd degree
+            double ev = cf[de], od = cf[dod];
 #pragma unroll
-            for (int d = D - 1; d >= 0; --d) v = fma(v, sv, cf[d]);
-            row[(rel + p) & 31] = v;
+            for (int d = de - 2; d >= 0; d -= 2) ev = fma(ev, s2, cf[d]);
+#pragma unroll
+            for (int d = dod - 2; d >= 1; d -= 2) od = fma(od, s2, cf[d]);
+            row[(rel + p) & 31] = fma(sv, od, ev);
+            row[(rel + NS - 1 - p) & 31] = fma(-sv, od, ev);
           }
         }
       } else if (has) {  // W_p = A g^p C_p stored at slot (rel + p) mod 32 of the point's row;
