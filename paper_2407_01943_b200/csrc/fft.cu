@@ -135,7 +135,7 @@ __device__ inline void group_bar(int id) {
 }
 
 template <int R0, bool SWZ, typename T2, int NT = kFftThreads>
-__device__ inline void fft16_regs(T2 (&v)[16], T2* buf, int lgL, int lgNfft, int es, int fs,
+__device__ __forceinline__ void fft16_regs(T2 (&v)[16], T2* buf, int lgL, int lgNfft, int es, int fs,
                                   const T2* __restrict__ tw, int& f_out, int& out0, int& step_out, int bar = 0,
                                   int tid = -1) {
   if (tid < 0) tid = threadIdx.x;
@@ -197,7 +197,7 @@ __device__ inline void fft16_regs(T2 (&v)[16], T2* buf, int lgL, int lgNfft, int
 
 // Stage-0 input index of register slot (bb, q) for this thread: element j + q*L/R0 of FFT f.
 template <int R0, int NT = kFftThreads>
-__device__ inline void stage0_index(int slot, int lgL, int lgNfft, int& f, int& e, int tid = -1) {
+__device__ __forceinline__ void stage0_index(int slot, int lgL, int lgNfft, int& f, int& e, int tid = -1) {
   if (tid < 0) tid = threadIdx.x;
   constexpr int lgR0 = R0 == 16 ? 4 : R0 == 8 ? 3 : R0 == 4 ? 2 : 1;
   const int bb = slot / R0, q = slot % R0;
@@ -274,7 +274,9 @@ __global__ void __launch_bounds__(kFftThreads, 2) fft_cols_kernel(
 // Pass A over the blocked grid with register loads: one tile (R rows x CW columns, contiguous,
 // NT * 16 elements) per CTA, several CTAs per SM in flight instead of a persistent bulk-copy
 // pipeline.  Rows outside the occupied interval are zeros and are not read.
-template <typename Real, int R0, int NT>
+// LGR > 0: the column length R = 2^LGR is a compile-time constant (every shared-memory and
+// register-slot index of the in-CTA FFT folds to an immediate); 0 = runtime R.
+template <typename Real, int R0, int NT, int LGR = 0>
 __global__ void __launch_bounds__(NT, NT == 128 ? 4 : NT == 256 ? 2 : 1) fft_cols_blk_kernel(
     const typename C2<Real>::T* __restrict__ grid, typename C2<Real>::T* __restrict__ out, int64_t mr, int R, int C,
     int CW, int k, int kpad, const typename C2<Real>::T* __restrict__ tw_r,
@@ -283,7 +285,14 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 4 : NT == 256 ? 2 : 1) fft_col
   using T2 = typename C2<Real>::T;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T2* const buf = reinterpret_cast<T2*>(smem_raw);  // [R][CW]
-  const int lgR = __ffs(R) - 1, lgCW = __ffs(CW) - 1, lg_nblk = __ffs(C / CW) - 1;
+  constexpr int kLgTile = NT == 128 ? 11 : NT == 256 ? 12 : 13;
+  if constexpr (LGR > 0) {
+    R = 1 << LGR;
+    CW = 1 << (kLgTile - LGR);
+  }
+  const int lgR = LGR > 0 ? LGR : __ffs(R) - 1;
+  const int lgCW = LGR > 0 ? kLgTile - LGR : __ffs(CW) - 1;
+  const int lg_nblk = __ffs(C) - 1 - lgCW;
   const int t = blockIdx.x;
   const int blk = t & ((1 << lg_nblk) - 1), ck = t >> lg_nblk;
   const int ch = ck / k, kk = ck - ch * k;
@@ -321,6 +330,7 @@ __host__ __device__ constexpr int crop_q(int c) { return c < 5 ? c : c + 7; }
 
 // NT threads per row: 256 for C = 4096 (2 CTAs / SM), 128 for C = 2048 (4 CTAs / SM, twice the
 // rows in flight to cover the row loads).
+// C = NT * 16 is fixed by NT, so every index of the in-CTA FFT is a compile-time constant
 template <typename Real, typename PReal, int R0, int NT = kFftThreads>
 __global__ void __launch_bounds__(NT, NT == 128 ? 4 : NT == 256 ? 2 : 1) fft_rows_crop_kernel(
     const typename C2<Real>::T* __restrict__ grid, int64_t mr, int R, int C, int RPC, int64_t kpad,
@@ -332,7 +342,8 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 4 : NT == 256 ? 2 : 1) fft_row
   T2* const buf = reinterpret_cast<T2*>(smem_raw);  // [C] (swizzled)
   const int k1 = blockIdx.x;                        // one row per CTA
   const int64_t ch = blockIdx.y;
-  const int lgC = __ffs(C) - 1;
+  constexpr int lgC = NT == 128 ? 11 : NT == 256 ? 12 : 13;
+  C = 1 << lgC;
   // Mr >= 2 nc, so the crop keeps k2 <= C/4 or k2 >= 3C/4 only: of this thread's outputs
   // k2 = out0 + q C/16 that is q in {0..4, 12..15} (kCropQ); the other seven are never formed
   Real acc[kCropN];
@@ -792,6 +803,13 @@ void fused_fft_prepare(Plan& plan) {
     NUS_ATTR((fft_cols_blk_kernel<double, 8, kFftThreads>));
     NUS_ATTR((fft_cols_blk_kernel<double, 4, kFftThreads>));
     NUS_ATTR((fft_cols_blk_kernel<double, 2, kFftThreads>));
+    NUS_ATTR((fft_cols_blk_kernel<double, 4, kFftThreads, 6>));
+    NUS_ATTR((fft_cols_blk_kernel<double, 8, kFftThreads, 7>));
+    NUS_ATTR((fft_cols_blk_kernel<double, 16, kFftThreads, 8>));
+    NUS_ATTR((fft_cols_blk_kernel<double, 2, kFftThreads, 9>));
+    NUS_ATTR((fft_cols_blk_kernel<double, 4, kFftThreads, 10>));
+    NUS_ATTR((fft_cols_blk_kernel<double, 8, kFftThreads, 11>));
+    NUS_ATTR((fft_cols_blk_kernel<double, 16, kFftThreads, 12>));
 #undef NUS_ATTR
     const int smem_w = 2 * kFftElems * static_cast<int>(sizeof(double2));
 #define NUS_ATTRW(KERN) NUS_CUDA(cudaFuncSetAttribute(KERN, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_w))
@@ -854,8 +872,9 @@ void launch_cols(const Plan& plan, void* grid, void* scratch, int64_t k, int64_t
   if (use_async(f, sizeof(T2)) && f.cols_mode != 2) {
     const int64_t ntiles = p.channels * k * (f.C / f.CW);
     auto* out = static_cast<T2*>(scratch);
-#define NUS_COLS_REG(R0, NT)                                                                                 \
-  launch_pdl(fft_cols_blk_kernel<Real, R0, NT>, dim3(static_cast<unsigned>(ntiles)), dim3(NT),                \
+#define NUS_COLS_REG(R0, NT) NUS_COLS_REGL(R0, NT, 0)
+#define NUS_COLS_REGL(R0, NT, LG)                                                                            \
+  launch_pdl(fft_cols_blk_kernel<Real, R0, NT, LG>, dim3(static_cast<unsigned>(ntiles)), dim3(NT),            \
              static_cast<size_t>(NT) * 16 * sizeof(T2), s, static_cast<const T2*>(g), out, p.mr, f.R, f.C, f.CW, \
              static_cast<int>(k), static_cast<int>(kpad), tr, th, tl, f.lo_bits, f.row_lo, f.row_cnt)
     if (f.cols_mode == 3) {
@@ -867,12 +886,23 @@ void launch_cols(const Plan& plan, void* grid, void* scratch, int64_t k, int64_t
       else if (r0 == 4) NUS_COLS_REG(4, 128);
       else NUS_COLS_REG(2, 128);
     } else {
-      if (r0 == 16) NUS_COLS_REG(16, kFftThreads);
-      else if (r0 == 8) NUS_COLS_REG(8, kFftThreads);
-      else if (r0 == 4) NUS_COLS_REG(4, kFftThreads);
-      else NUS_COLS_REG(2, kFftThreads);
+      switch (f.R) {  // the column lengths of the configs (Mr = 2^17 .. 2^24), compile-time shapes
+        case 64: NUS_COLS_REGL(4, kFftThreads, 6); break;
+        case 128: NUS_COLS_REGL(8, kFftThreads, 7); break;
+        case 256: NUS_COLS_REGL(16, kFftThreads, 8); break;
+        case 512: NUS_COLS_REGL(2, kFftThreads, 9); break;
+        case 1024: NUS_COLS_REGL(4, kFftThreads, 10); break;
+        case 2048: NUS_COLS_REGL(8, kFftThreads, 11); break;
+        case 4096: NUS_COLS_REGL(16, kFftThreads, 12); break;
+        default:
+          if (r0 == 16) NUS_COLS_REG(16, kFftThreads);
+          else if (r0 == 8) NUS_COLS_REG(8, kFftThreads);
+          else if (r0 == 4) NUS_COLS_REG(4, kFftThreads);
+          else NUS_COLS_REG(2, kFftThreads);
+      }
     }
 #undef NUS_COLS_REG
+#undef NUS_COLS_REGL
     return;
   }
   if (use_async(f, sizeof(T2))) {
