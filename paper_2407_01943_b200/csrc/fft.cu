@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(kFftThreads, 2) fft_cols_kernel(
 // LGR > 0: the column length R = 2^LGR is a compile-time constant (every shared-memory and
 // register-slot index of the in-CTA FFT folds to an immediate); 0 = runtime R.
 template <typename Real, int R0, int NT, int LGR = 0>
-__global__ void __launch_bounds__(NT, NT == 128 ? 4 : NT == 256 ? 2 : 1) fft_cols_blk_kernel(
+__global__ void __launch_bounds__(NT, NT == 128 ? 4 : NT == 256 ? (sizeof(Real) == 4 ? 3 : 2) : 1) fft_cols_blk_kernel(
     const typename C2<Real>::T* __restrict__ grid, typename C2<Real>::T* __restrict__ out, int64_t mr, int R, int C,
     int CW, int k, int kpad, const typename C2<Real>::T* __restrict__ tw_r,
     const typename C2<Real>::T* __restrict__ tw_hi, const typename C2<Real>::T* __restrict__ tw_lo, int lo_bits,
@@ -332,7 +332,7 @@ __host__ __device__ constexpr int crop_q(int c) { return c < 5 ? c : c + 7; }
 // rows in flight to cover the row loads).
 // C = NT * 16 is fixed by NT, so every index of the in-CTA FFT is a compile-time constant
 template <typename Real, typename PReal, int R0, int NT = kFftThreads>
-__global__ void __launch_bounds__(NT, NT == 128 ? 4 : NT == 256 ? 2 : 1) fft_rows_crop_kernel(
+__global__ void __launch_bounds__(NT, NT == 128 ? (sizeof(Real) == 4 ? 6 : 4) : NT == 256 ? (sizeof(Real) == 4 ? 3 : 2) : 1) fft_rows_crop_kernel(
     const typename C2<Real>::T* __restrict__ grid, int64_t mr, int R, int C, int RPC, int64_t kpad,
     int k_count, int64_t nc, int64_t mode_offset, const Real* __restrict__ deconv,
     const typename C2<Real>::T* __restrict__ tw_c, typename C2<Real>::T* __restrict__ j_out,
