@@ -210,6 +210,12 @@ int nus_mtnufft_spread_device(nus_mtnufft_t est, const void* x_dev, int32_t x_dt
                               int64_t s1, void* grid_dev, int64_t k_pad, void* stream);
 int nus_mtnufft_transform_device(nus_mtnufft_t est, void* grid_dev, int64_t k0, int64_t k1,
                                  double divisor, int32_t accumulate, void* power_dev, void* stream);
+/* Occupied pass-A rows of the fused FFT's blocked grid: the spread writes and pass A reads only
+ * rows [row_lo, row_lo + row_cnt) (cyclic, of nrows) that this estimator's own samples touch.
+ * A sample split must widen every rank's interval to the union over ranks before grids are
+ * summed (set: the new interval must contain the current one; nrows = 0 when not blocked). */
+int nus_mtnufft_grid_rows(nus_mtnufft_t est, int32_t* row_lo, int32_t* row_cnt, int32_t* nrows);
+int nus_mtnufft_set_grid_rows(nus_mtnufft_t est, int32_t row_lo, int32_t row_cnt);
 /* Per-stage CUDA-event timing of the fast path: record (on the caller's stream) the
  * next max_runs estimate calls; _read syncs and returns summed ms for
  * [spread, fft, crop+power] and the number of runs recorded. */

@@ -99,6 +99,8 @@ _SIGS = {
     "nus_device_info": [ctypes.c_int, _i32p, _i32p, _i32p, _i64p],
     "nus_kernel_launch_count": [],
     "nus_set_spread_kernel": [_i32],
+    "nus_mtnufft_grid_rows": [_vp, _i32p, _i32p, _i32p],
+    "nus_mtnufft_set_grid_rows": [_vp, _i32, _i32],
     "nus_get_spread_kernel": [_i32p],
     "nus_plan_create": [_dp, _i64, _dp, _i64, _d, _i32, _i32, _i32, _i32, ctypes.POINTER(_vp)],
     "nus_plan_destroy": [_vp],

@@ -575,6 +575,35 @@ int nus_mtnufft_transform_device(nus_mtnufft_t est, void* grid_dev, int64_t k0, 
   });
 }
 
+int nus_mtnufft_grid_rows(nus_mtnufft_t est, int32_t* row_lo, int32_t* row_cnt, int32_t* nrows) {
+  return guarded([&] {
+    nus::require(est && row_lo && row_cnt && nrows, "grid_rows: null argument");
+    const auto& f = est->est->plan->ffft;
+    const bool blk = f.ready && f.blocked;
+    *row_lo = blk ? f.row_lo : 0;
+    *row_cnt = blk ? f.row_cnt : 0;
+    *nrows = blk ? f.R : 0;
+  });
+}
+
+int nus_mtnufft_set_grid_rows(nus_mtnufft_t est, int32_t row_lo, int32_t row_cnt) {
+  return guarded([&] {
+    nus::require(est != nullptr, "set_grid_rows: null argument");
+    auto& f = est->est->plan->ffft;
+    if (!(f.ready && f.blocked)) return;
+    nus::require(row_lo >= 0 && row_lo < f.R && row_cnt >= 1 && row_cnt <= f.R, "set_grid_rows: bad interval");
+    // every currently occupied row r (cyclic offset from row_lo < row_cnt) must stay inside
+    for (int q = 0; q < f.row_cnt; ++q) {
+      const int r = (f.row_lo + q) % f.R;
+      nus::require(((r - row_lo) % f.R + f.R) % f.R < row_cnt,
+                   "set_grid_rows: the interval must contain the estimator's occupied rows");
+    }
+    std::lock_guard<std::mutex> lock(est->est->plan->mu);
+    f.row_lo = row_lo;
+    f.row_cnt = row_cnt;
+  });
+}
+
 int nus_mtnufft_timing(nus_mtnufft_t est, int64_t max_runs) {
   return guarded([&] {
     nus::require(est && max_runs >= 0, "nus_mtnufft_timing: bad argument");

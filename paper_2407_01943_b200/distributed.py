@@ -35,6 +35,25 @@ def split_range(n: int, world: int, rank: int):
     return n * rank // world, n * (rank + 1) // world
 
 
+def covering_interval(occupied) -> tuple:
+    """Smallest cyclic interval (start, length) holding every True of ``occupied``: the
+    complement of its longest cyclic run of False (plan.cu's rule for one estimator)."""
+    occ = np.asarray(occupied, dtype=bool)
+    nr = occ.size
+    if occ.all() or not occ.any():
+        return 0, nr
+    best_len, best_end = 0, 0
+    for start in range(nr):
+        if occ[start] or not occ[(start - 1) % nr]:
+            continue
+        length = 0
+        while length < nr and not occ[(start + length) % nr]:
+            length += 1
+        if length > best_len:
+            best_len, best_end = length, (start + length) % nr
+    return best_end, nr - best_len
+
+
 def balanced_triangle_rows(n: int, world: int):
     """Row boundaries so each rank gets ~equal work in the upper-triangle sum
     sum_n (2F w_n^2 + 2 sum_{m>n} ...): row n costs (n_total - n) pairs."""
@@ -102,6 +121,14 @@ class DeviceEngine:
     def transform(self, est, grid_rows, k0, k1, divisor, power):
         C.check(C.lib().nus_mtnufft_transform_device(est.h, grid_rows.data_ptr(), k0, k1, divisor, 0,
                                                      power.data_ptr(), self._stream()))
+
+    def grid_rows(self, est):
+        lo, cnt, nr = C._i32(), C._i32(), C._i32()
+        C.check(C.lib().nus_mtnufft_grid_rows(est.h, ctypes.byref(lo), ctypes.byref(cnt), ctypes.byref(nr)))
+        return lo.value, cnt.value, nr.value
+
+    def set_grid_rows(self, est, lo, cnt):
+        C.check(C.lib().nus_mtnufft_set_grid_rows(est.h, int(lo), int(cnt)))
 
     def mr(self, est):
         return int(est.info.mr)
@@ -198,6 +225,8 @@ class SampleSplit:
         self.tapers = tapers
         self.est = self.engine.create(times[self.s0:self.s1], centers, f_max, f_w, k, eps, precision,
                                       tapers[:, self.s0:self.s1])
+        if self.world > 1:  # partial grids are summed: every rank covers the union of occupied rows
+            self._widen_rows()
         self.kpad = int(math.ceil(k / self.world)) * self.world
         self.per_rank = self.kpad // self.world
         self.mr = self.engine.mr(self.est)
@@ -206,6 +235,22 @@ class SampleSplit:
         self.grid = self.engine.zeros((self.kpad, self.mr * 2), self.real)
         self.owned = self.engine.zeros((self.per_rank, self.mr * 2), self.real)
         self.nc = len(centers)
+
+    def _widen_rows(self):
+        """Union of the ranks' occupied pass-A rows (a cyclic interval each) -> every rank."""
+        if not hasattr(self.engine, "grid_rows"):
+            return
+        import torch
+        lo, cnt, nr = self.engine.grid_rows(self.est)
+        if nr == 0:
+            return
+        occ = torch.zeros(nr, dtype=torch.float64)
+        occ[(lo + np.arange(cnt)) % nr] = 1.0
+        if self.engine.__class__.__name__ == "DeviceEngine":
+            occ = occ.to(self.engine.dev)
+        self.dist.all_reduce(occ, op=self.dist.ReduceOp.MAX, group=self.group)
+        new_lo, new_cnt = covering_interval(occ.cpu().numpy() > 0)
+        self.engine.set_grid_rows(self.est, new_lo, new_cnt)
 
     def _normalised_tapers(self, times, f_max, f_w, k):
         """Interpolated DPSS on the full grid + row-split R(B) normalisation (all_reduce of K sums)."""

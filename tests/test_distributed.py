@@ -210,3 +210,13 @@ def test_balanced_triangle_rows_partition():
         assert b[0] == 0 and b[-1] == n and all(x <= y for x, y in zip(b, b[1:]))
         work = [sum(n - i for i in range(b[r], b[r + 1])) for r in range(g)]
         assert max(work) - min(work) <= n + 1
+
+
+def test_covering_interval_cyclic():
+    occ = np.zeros(16, dtype=bool)
+    occ[[3, 4, 5, 9]] = True
+    assert D.covering_interval(occ) == (3, 7)
+    occ = np.zeros(16, dtype=bool)
+    occ[[0, 1, 14, 15]] = True  # wraps
+    assert D.covering_interval(occ) == (14, 4)
+    assert D.covering_interval(np.ones(8, dtype=bool)) == (0, 8)

@@ -61,3 +61,51 @@ def test_taper_and_channel_shard_device_engine(nccl_group):
     for ch in range(3):
         ref = C.mtnufft_power(c3.times[ch], wc[ch], c3.values[ch], centers, 1e-9)
         assert rel_l2(allp[ch], ref) <= 1e-4
+
+
+@pytest.mark.parametrize("kern", ["gaussian", "es"])
+@pytest.mark.parametrize("ranks", [2, 4])
+def test_sample_split_emulated_ranks_on_one_gpu(kern, ranks):
+    """The sample split's device path with G ranks emulated on one GPU (no collective: the
+    reduce-scatter is a sum of the G partial grids): each chunk's estimator occupies different
+    pass-A rows (C2-like Poisson times span half the grid period), so the row intervals are
+    widened to their union first (nus_mtnufft_set_grid_rows); P equals the single-GPU P."""
+    import torch
+    wl = W.c2(n=1 << 18)
+    eng = D.DeviceEngine()
+    full = eng.create(wl.times, wl.centers, wl.f_max, float(wl.f_w[0]), 7, 1e-9, "f64", None)
+    w = full.tapers()[0]
+    p_full = full.power(wl.values)[0]
+    kpad = -(-7 // ranks) * ranks
+    per = kpad // ranks
+    parts, rows = [], []
+    for r in range(ranks):
+        s0, s1 = D.split_range(wl.n, ranks, r)
+        e = eng.create(wl.times[s0:s1], wl.centers, wl.f_max, float(wl.f_w[0]), 7, 1e-9, "f64", w[:, s0:s1])
+        parts.append((e, s0, s1))
+        rows.append(eng.grid_rows(e))
+    nr = rows[0][2]
+    assert nr > 0 and len({(lo, cnt) for lo, cnt, _ in rows}) > 1  # the chunks occupy different rows
+    occ = np.zeros(nr, dtype=bool)
+    for lo, cnt, _ in rows:
+        occ[(lo + np.arange(cnt)) % nr] = True
+    lo, cnt = D.covering_interval(occ)
+    mr = eng.mr(full)
+    total = torch.zeros((kpad, 2 * mr), dtype=torch.float64, device="cuda")
+    for e, s0, s1 in parts:
+        eng.set_grid_rows(e, lo, cnt)
+        g = torch.zeros((kpad, 2 * mr), dtype=torch.float64, device="cuda")
+        x = torch.as_tensor(wl.values[s0:s1], device="cuda")
+        eng.spread(e, x, 0, s1 - s0, g, kpad)
+        total += g
+    power = torch.zeros(wl.centers.size, dtype=torch.float64, device="cuda")
+    for r, (e, _, _) in enumerate(parts):
+        k0, k1 = r * per, min(7, (r + 1) * per)
+        if k1 > k0:
+            owned = total[k0:k0 + per].contiguous()
+            pr = torch.zeros_like(power)
+            eng.transform(e, owned, k0, k1, 1.0, pr)
+            power += pr
+    torch.cuda.synchronize()
+    p = power.cpu().numpy() / 7.0
+    assert rel_l2(p, p_full) < 1e-12
