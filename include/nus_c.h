@@ -214,6 +214,22 @@ int nus_mtnufft_transform_device(nus_mtnufft_t est, void* grid_dev, int64_t k0, 
  * rows [row_lo, row_lo + row_cnt) (cyclic, of nrows) that this estimator's own samples touch.
  * A sample split must widen every rank's interval to the union over ranks before grids are
  * summed (set: the new interval must contain the current one; nrows = 0 when not blocked). */
+/* The sample split's spread fused with its exchange: samples [s0,s1) are spread and taper k is
+ * stored straight into slot_ptrs_dev[k / per] + (k % per) * Mr (a device array of G pointers
+ * to the owners' receive slots for this rank; peer NVLink addresses from nus_ipc_open_handle on
+ * a multi-GPU box), so the transfer overlaps the spread segment by segment instead of following
+ * it as a reduce-scatter.  One channel. */
+int nus_mtnufft_spread_slots_device(nus_mtnufft_t est, const void* x_dev, int32_t x_dtype, int64_t s0,
+                                    int64_t s1, const void* slot_ptrs_dev, int64_t per, void* stream);
+/* out = sum over nslots slots (slot q at base + q * slot_stride complex elements) of count complex
+ * elements, in slot order (deterministic); precision = enum nus_precision. */
+int nus_sum_slots_device(const void* base, int64_t nslots, int64_t slot_stride, int64_t count, void* out,
+                         int32_t precision, void* stream);
+/* CUDA IPC for the receive slots: 64-byte handle of a device allocation, and a peer mapping of
+ * another process's handle (close with nus_ipc_close). */
+int nus_ipc_get_handle(const void* dev_ptr, void* handle64);
+int nus_ipc_open(const void* handle64, int32_t device, void** dev_ptr);
+int nus_ipc_close(void* dev_ptr);
 int nus_mtnufft_grid_rows(nus_mtnufft_t est, int32_t* row_lo, int32_t* row_cnt, int32_t* nrows);
 int nus_mtnufft_set_grid_rows(nus_mtnufft_t est, int32_t row_lo, int32_t row_cnt);
 /* Per-stage CUDA-event timing of the fast path: record (on the caller's stream) the

@@ -100,6 +100,11 @@ _SIGS = {
     "nus_kernel_launch_count": [],
     "nus_set_spread_kernel": [_i32],
     "nus_mtnufft_grid_rows": [_vp, _i32p, _i32p, _i32p],
+    "nus_mtnufft_spread_slots_device": [_vp, _vp, _i32, _i64, _i64, _vp, _i64, _vp],
+    "nus_sum_slots_device": [_vp, _i64, _i64, _i64, _vp, _i32, _vp],
+    "nus_ipc_get_handle": [_vp, _vp],
+    "nus_ipc_open": [_vp, _i32, ctypes.POINTER(_vp)],
+    "nus_ipc_close": [_vp],
     "nus_mtnufft_set_grid_rows": [_vp, _i32, _i32],
     "nus_get_spread_kernel": [_i32p],
     "nus_plan_create": [_dp, _i64, _dp, _i64, _d, _i32, _i32, _i32, _i32, ctypes.POINTER(_vp)],

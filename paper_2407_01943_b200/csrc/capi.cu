@@ -575,6 +575,64 @@ int nus_mtnufft_transform_device(nus_mtnufft_t est, void* grid_dev, int64_t k0, 
   });
 }
 
+int nus_mtnufft_spread_slots_device(nus_mtnufft_t est, const void* x_dev, int32_t x_dtype, int64_t s0,
+                                    int64_t s1, const void* slot_ptrs_dev, int64_t per, void* stream) {
+  return guarded([&] {
+    nus::require(est && x_dev && slot_ptrs_dev, "spread_slots_device: null argument");
+    auto& e = *est->est;
+    nus::require(e.plan->p.path == NUS_PATH_FAST, "spread_slots_device: estimator is on the direct path");
+    nus::require(e.cfg.channels == 1, "spread_slots_device: one channel");
+    nus::require(per >= 1, "spread_slots_device: per must be >= 1");
+    nus::require(0 <= s0 && s0 <= s1 && s1 <= e.cfg.n, "spread_slots_device: bad sample range");
+    nus::use_device(e.cfg.device);
+    nus::SpreadArgs a;
+    a.x = x_dev;
+    a.x_dtype = x_dtype;
+    a.tapers = e.tapers_sorted.ptr;
+    a.k = e.cfg.k_tapers;
+    a.kpad = e.cfg.k_tapers;
+    a.s0 = s0;
+    a.s1 = s1;
+    a.grid = nullptr;
+    a.slots = static_cast<void* const*>(const_cast<void*>(slot_ptrs_dev));
+    a.per = per;
+    nus::launch_spread(*e.plan, a, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int nus_sum_slots_device(const void* base, int64_t nslots, int64_t slot_stride, int64_t count, void* out,
+                         int32_t precision, void* stream) {
+  return guarded([&] {
+    nus::require(base && out && nslots >= 1 && count >= 0 && slot_stride >= count, "sum_slots: bad argument");
+    nus::require(precision == NUS_F64 || precision == NUS_F32, "sum_slots: unknown precision");
+    nus::sum_slots(base, nslots, slot_stride, count, out, precision == NUS_F64, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int nus_ipc_get_handle(const void* dev_ptr, void* handle64) {
+  return guarded([&] {
+    nus::require(dev_ptr && handle64, "ipc: null argument");
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    cudaIpcMemHandle_t h;
+    NUS_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
+    std::memcpy(handle64, &h, sizeof(h));
+  });
+}
+
+int nus_ipc_open(const void* handle64, int32_t device, void** dev_ptr) {
+  return guarded([&] {
+    nus::require(handle64 && dev_ptr, "ipc: null argument");
+    nus::use_device(device);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, sizeof(h));
+    NUS_CUDA(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+
+int nus_ipc_close(void* dev_ptr) {
+  return guarded([&] { NUS_CUDA(cudaIpcCloseMemHandle(dev_ptr)); });
+}
+
 int nus_mtnufft_grid_rows(nus_mtnufft_t est, int32_t* row_lo, int32_t* row_cnt, int32_t* nrows) {
   return guarded([&] {
     nus::require(est && row_lo && row_cnt && nrows, "grid_rows: null argument");

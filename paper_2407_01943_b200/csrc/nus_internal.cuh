@@ -194,8 +194,16 @@ struct SpreadArgs {
   int64_t kpad = 1;
   int64_t s0 = 0, s1 = -1;
   void* grid = nullptr;
+  // sample split fused with its exchange (one channel): taper k is written to
+  // slots[k / per] + (k % per) * Mr instead of grid + k * Mr -- the owner's receive slot for
+  // this rank, a peer (NVLink) address on a multi-GPU box.  Device array of pointers.
+  void* const* slots = nullptr;
+  int64_t per = 0;
 };
 void launch_spread(const Plan& plan, const SpreadArgs& a, cudaStream_t s);
+// out[i] = sum_{s < nslots} slots[s][i] over `count` complex elements (fixed order: deterministic)
+void sum_slots(const void* base, int64_t nslots, int64_t slot_stride, int64_t count, void* out, bool f64,
+               cudaStream_t s);
 
 // FFT of rows [C][kpad][Mr] (first k rows per channel are transformed), then crop:
 // optional J [C][k][I] = deconv * B[bin] and power [C][I] (+)= sum_k |J|^2 / divisor.

@@ -65,6 +65,8 @@ struct SpreadParams {
   const Real* taper_base;  // tapers, or a device constant 1 with zero strides
   int64_t tstride_k, tstride_j;
   const int32_t* seg_ranges;
+  typename Vec2<Real>::T* const* slots;  // fused sample-split exchange (SpreadArgs::slots) or null
+  int64_t per;
   int tile, w, w2, k0, kg, x_dtype, x_complex;
   Real beta, cq[kMaxW2];
   // tensor-core staging: W_{p+2} = W_p * q_p, q_{p+2} = q_p * ve (even / odd chains)
@@ -520,6 +522,11 @@ __global__ void __launch_bounds__(kTcWarps * 32, G == 1 ? kTcCtasPerSm : 3) spre
       for (int gg = 0; gg < G; ++gg) {
         R2* out0 = out + off_h0 + static_cast<int64_t>(8 * gg) * P.mr;
         R2* out1 = out + off_h1 + static_cast<int64_t>(8 * gg) * P.mr;
+        if (P.slots) {  // taper k -> owner k / per, its slot row k % per (possibly a peer GPU)
+          const int64_t ka = P.k0 + 8 * gg + 2 * t, kb = ka + 1;
+          out0 = P.slots[ka / P.per] + (ka % P.per) * P.mr;
+          out1 = P.slots[kb / P.per] + (kb % P.per) * P.mr;
+        }
         const bool k0ok = 8 * gg + 2 * t < P.kg, k1ok = 8 * gg + 2 * t + 1 < P.kg;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
@@ -535,6 +542,7 @@ __global__ void __launch_bounds__(kTcWarps * 32, G == 1 ? kTcCtasPerSm : 3) spre
     n1 = n2;
     tc_advance(n2, pre, pp, P, stride);
   }
+  if (P.slots) __threadfence_system();  // peer-slot stores ordered before the caller's barrier
 }
 
 void es_upload() {  // once per device
@@ -673,6 +681,9 @@ void spread_typed(const Plan& plan, const SpreadArgs& a, cudaStream_t s) {
   P.tapers = static_cast<const Real*>(a.tapers);
   P.x = a.x;
   P.grid = static_cast<typename Vec2<Real>::T*>(a.grid);
+  P.slots = reinterpret_cast<typename Vec2<Real>::T* const*>(a.slots);
+  P.per = a.per;
+  require(!a.slots || (p.channels == 1 && a.per >= 1), "spread: slot output needs one channel and per >= 1");
   P.n = p.n;
   P.mr = p.mr;
   P.ntiles = tb.ntiles;
@@ -710,6 +721,7 @@ void spread_typed(const Plan& plan, const SpreadArgs& a, cudaStream_t s) {
   // the tensor-core kernel's weight rows hold one 32-cell window: wider Gaussians (eps < ~2e-13,
   // 2w > 32) take the gather kernel; the ES window is at most 16 cells
   const bool tc = use_tc && p.sw <= 32;
+  require(!a.slots || tc, "spread: slot output needs the tensor-core kernel");
   const int ns = p.kernel == NUS_KERNEL_ES ? p.sw : 0;
   const int64_t k = a.tapers ? a.k : 1;
   // 9..16 tapers of a real series: both groups from one staging of the points
@@ -754,6 +766,38 @@ void spread_typed(const Plan& plan, const SpreadArgs& a, cudaStream_t s) {
 const char* spread_kernel_name() {
   const char* e = std::getenv("NUS_SPREAD");
   return (e && std::strcmp(e, "gather") == 0) ? "spread_gather_kernel" : "spread_tc_kernel";
+}
+
+namespace {
+
+template <typename T2>
+__global__ void sum_slots_kernel(const T2* __restrict__ base, int64_t nslots, int64_t stride, int64_t count,
+                                 T2* __restrict__ out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    T2 acc = base[i];
+    for (int64_t q = 1; q < nslots; ++q) {
+      const T2 v = base[q * stride + i];
+      acc.x += v.x;
+      acc.y += v.y;
+    }
+    out[i] = acc;
+  }
+}
+
+}  // namespace
+
+void sum_slots(const void* base, int64_t nslots, int64_t slot_stride, int64_t count, void* out, bool f64,
+               cudaStream_t s) {
+  const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((count + 255) / 256, 148 * 8));
+  if (f64)
+    sum_slots_kernel<double2><<<blocks, 256, 0, s>>>(static_cast<const double2*>(base), nslots, slot_stride, count,
+                                                     static_cast<double2*>(out));
+  else
+    sum_slots_kernel<float2><<<blocks, 256, 0, s>>>(static_cast<const float2*>(base), nslots, slot_stride, count,
+                                                    static_cast<float2*>(out));
+  note_launch();
+  check_launch("sum_slots_kernel");
 }
 
 void launch_spread(const Plan& plan, const SpreadArgs& a, cudaStream_t s) {

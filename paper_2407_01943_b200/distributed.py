@@ -122,6 +122,25 @@ class DeviceEngine:
         C.check(C.lib().nus_mtnufft_transform_device(est.h, grid_rows.data_ptr(), k0, k1, divisor, 0,
                                                      power.data_ptr(), self._stream()))
 
+    def spread_slots(self, est, x, s0, s1, slot_ptrs, per):
+        C.check(C.lib().nus_mtnufft_spread_slots_device(est.h, x.data_ptr(), 1 if x.dtype == self.torch.float32 else 0,
+                                                        s0, s1, slot_ptrs.data_ptr(), per, self._stream()))
+
+    def sum_slots(self, base, nslots, slot_stride, count, out):
+        prec = 1 if base.dtype == self.torch.float32 else 0
+        C.check(C.lib().nus_sum_slots_device(base.data_ptr(), nslots, slot_stride, count, out.data_ptr(), prec,
+                                             self._stream()))
+
+    def ipc_handle(self, t) -> bytes:
+        buf = ctypes.create_string_buffer(64)
+        C.check(C.lib().nus_ipc_get_handle(t.data_ptr(), buf))
+        return buf.raw
+
+    def ipc_open(self, handle: bytes) -> int:
+        p = ctypes.c_void_p()
+        C.check(C.lib().nus_ipc_open(ctypes.create_string_buffer(handle, 64), self.device, ctypes.byref(p)))
+        return int(p.value)
+
     def grid_rows(self, est):
         lo, cnt, nr = C._i32(), C._i32(), C._i32()
         C.check(C.lib().nus_mtnufft_grid_rows(est.h, ctypes.byref(lo), ctypes.byref(cnt), ctypes.byref(nr)))
@@ -209,7 +228,7 @@ class SampleSplit:
     """Config C4: one long series, samples split across ranks, reduce-scatter of fine grids."""
 
     def __init__(self, times, centers, f_max, f_w, k, eps, precision="f64", engine=None, group=None,
-                 tapers: Optional[np.ndarray] = None):
+                 tapers: Optional[np.ndarray] = None, fused: Optional[bool] = None):
         import torch.distributed as dist
         self.dist = dist
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -231,10 +250,37 @@ class SampleSplit:
         self.per_rank = self.kpad // self.world
         self.mr = self.engine.mr(self.est)
         self.real = self.engine.real_dtype(self.est)
-        # full local grid [kpad][Mr] complex as interleaved reals; padding rows stay zero
-        self.grid = self.engine.zeros((self.kpad, self.mr * 2), self.real)
-        self.owned = self.engine.zeros((self.per_rank, self.mr * 2), self.real)
         self.nc = len(centers)
+        self.owned = self.engine.zeros((self.per_rank, self.mr * 2), self.real)
+        # fused (default with the device engine): the spread stores each taper straight into its
+        # owner's receive slot for this rank over peer memory; else a full local grid and NCCL's
+        # reduce-scatter (the baseline, and the CPU test engine's path)
+        self.fused = hasattr(self.engine, "spread_slots") if fused is None else fused
+        if self.fused:
+            self._setup_slots()
+        else:
+            # full local grid [kpad][Mr] complex as interleaved reals; padding rows stay zero
+            self.grid = self.engine.zeros((self.kpad, self.mr * 2), self.real)
+
+    def _setup_slots(self):
+        """Receive slots [G][per][Mr] on every rank; this rank's slot pointer in every owner's
+        buffer (CUDA IPC peer mappings, exchanged with all_gather_object)."""
+        import torch
+        g, r, per, mr = self.world, self.rank, self.per_rank, self.mr
+        alloc = getattr(self.engine, "alloc_slots", self.engine.zeros)
+        self.recv = alloc((g, per, mr * 2), self.real)
+        csize = 2 * self.recv.element_size()
+        if g > 1:
+            handles = [None] * g
+            self.dist.all_gather_object(handles, self.engine.ipc_handle(self.recv), group=self.group)
+            self.peers = {o: self.engine.ipc_open(handles[o]) for o in range(g) if o != r}
+            bases = [self.recv.data_ptr() if o == r else self.peers[o] for o in range(g)]
+        else:
+            self.peers = {}
+            bases = [self.recv.data_ptr()]
+        ptrs = [b + r * per * mr * csize for b in bases]
+        self.slot_ptrs = torch.tensor(ptrs, dtype=torch.int64, device=self.recv.device)
+        self.flag = torch.zeros(1, dtype=self.real, device=self.recv.device)
 
     def _widen_rows(self):
         """Union of the ranks' occupied pass-A rows (a cyclic interval each) -> every rank."""
@@ -272,8 +318,15 @@ class SampleSplit:
 
     def estimate(self, x_local, power):
         """x_local: this rank's samples [s1-s0] on the device; rank 0 receives P in ``power``."""
-        self.engine.spread(self.est, x_local, 0, self.s1 - self.s0, self.grid, self.kpad)
-        self.dist.reduce_scatter_tensor(self.owned, self.grid, op=self.dist.ReduceOp.SUM, group=self.group)
+        if self.fused:
+            self.engine.spread_slots(self.est, x_local, 0, self.s1 - self.s0, self.slot_ptrs, self.per_rank)
+            if self.world > 1:  # stream-ordered barrier: every rank's slot stores have landed
+                self.dist.all_reduce(self.flag, op=self.dist.ReduceOp.SUM, group=self.group)
+            count = self.per_rank * self.mr
+            self.engine.sum_slots(self.recv, self.world, count, count, self.owned)
+        else:
+            self.engine.spread(self.est, x_local, 0, self.s1 - self.s0, self.grid, self.kpad)
+            self.dist.reduce_scatter_tensor(self.owned, self.grid, op=self.dist.ReduceOp.SUM, group=self.group)
         k0 = self.rank * self.per_rank
         k1 = min(self.k, k0 + self.per_rank)
         if k1 > k0:

@@ -115,6 +115,61 @@ class NumpyEngine:
         power.copy_(torch.as_tensor(self._power(est, g) / divisor))
 
 
+class SlotEngine(NumpyEngine):
+    """NumpyEngine plus the fused exchange's device interface, with file-backed shared mappings
+    standing in for CUDA IPC: a receive buffer is a memmap whose "handle" is its path, and a
+    "device pointer" is (registered base + byte offset), so the ranks' slot pointer arithmetic,
+    handle exchange, barrier and slot sums run exactly as SampleSplit drives them."""
+
+    def __init__(self, tmpdir, rank):
+        self.tmpdir, self.rank = tmpdir, rank
+        self.maps = {}  # base address -> float64 array (flat)
+
+    def _register(self, arr):
+        base = (len(self.maps) + 1) << 40
+        self.maps[base] = arr
+        return base
+
+    def alloc_slots(self, shape, dtype):
+        path = os.path.join(self.tmpdir, f"recv{self.rank}.bin")
+        mm = np.memmap(path, dtype=np.float64, mode="w+", shape=tuple(shape))
+        mm[:] = 0.0
+        mm.flush()
+        t = torch.from_numpy(mm)
+        self.own = (t, self._register(mm.reshape(-1)))
+        return t
+
+    def ipc_handle(self, t):
+        path = os.path.join(self.tmpdir, f"recv{self.rank}.bin").encode()
+        return path + b"\0" * (64 - len(path))
+
+    def ipc_open(self, handle):
+        path = handle.rstrip(b"\0").decode()
+        return self._register(np.memmap(path, dtype=np.float64, mode="r+").reshape(-1))
+
+    def _resolve(self, ptr):
+        if self.own[0].data_ptr() <= ptr < self.own[0].data_ptr() + self.own[0].numel() * 8:
+            return self.maps[self.own[1]], (ptr - self.own[0].data_ptr()) // 8
+        base = max(b for b in self.maps if b <= ptr)
+        return self.maps[base], (ptr - base) // 8
+
+    def spread_slots(self, est, x, s0, s1, slot_ptrs, per):
+        g = self._grid(est, 0, x.numpy(), s0, s1)
+        mr = g.shape[1]
+        for k in range(est.k):
+            arr, off = self._resolve(int(slot_ptrs[k // per]))
+            row = off + (k % per) * 2 * mr
+            arr[row:row + 2 * mr:2] = g[k].real
+            arr[row + 1:row + 2 * mr:2] = g[k].imag
+
+    def sum_slots(self, base, nslots, slot_stride, count, out):
+        flat = base.reshape(-1)
+        acc = torch.zeros(2 * count, dtype=torch.float64)
+        for q in range(nslots):
+            acc += flat[2 * q * slot_stride:2 * q * slot_stride + 2 * count]
+        out.view(-1).copy_(acc)
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -130,8 +185,11 @@ def _worker(rank, world, port, kind, q):
         wl = W.small(n=700, n_centers=256, k=3, nw=3.0, eps=1e-9, seed=5)
         eng = NumpyEngine()
         fw = float(wl.f_w[0])
-        if kind == "sample":
+        if kind in ("sample", "sample_fused"):
+            if kind == "sample_fused":
+                eng = SlotEngine(os.environ["NUS_TEST_SLOTDIR"], rank)
             ss = D.SampleSplit(wl.times, wl.centers, wl.f_max, fw, 3, 1e-9, engine=eng)
+            assert ss.fused == (kind == "sample_fused")
             xl = torch.as_tensor(wl.values[ss.s0:ss.s1].copy())
             pw = torch.zeros(wl.centers.size, dtype=torch.float64)
             ss.estimate(xl, pw)
@@ -184,6 +242,17 @@ def test_sample_split_reduce_scatter_matches_single_process():
     # row-split normalisation == full normalisation
     w_full, _ = C.gpss_interpolated(wl.times, wl.f_max, float(wl.f_w[0]), 3, threads=1)
     np.testing.assert_allclose(np.abs(tapers), np.abs(w_full), rtol=1e-9, atol=1e-15)
+    ref = C.mtnufft_power(wl.times, tapers, wl.values, wl.centers, 1e-9)
+    assert rel_l2(p, ref) < 1e-12
+
+
+def test_sample_split_fused_slot_exchange_matches_single_process(tmp_path, monkeypatch):
+    """World 2 (gloo): the fused exchange's host logic -- receive slots, handle exchange
+    (all_gather_object), per-owner slot pointers, the barrier, slot sums in rank order."""
+    monkeypatch.setenv("NUS_TEST_SLOTDIR", str(tmp_path))
+    p, tapers, kpad = _run("sample_fused")
+    assert kpad == 4
+    wl = W.small(n=700, n_centers=256, k=3, nw=3.0, eps=1e-9, seed=5)
     ref = C.mtnufft_power(wl.times, tapers, wl.values, wl.centers, 1e-9)
     assert rel_l2(p, ref) < 1e-12
 

@@ -30,10 +30,14 @@ def nccl_group():
     dist.destroy_process_group()
 
 
-def test_sample_split_device_engine(nccl_group):
+@pytest.mark.parametrize("fused", [True, False])
+def test_sample_split_device_engine(nccl_group, fused):
+    """World-1 NCCL group: the fused path (spread into receive slots + slot sum) and the
+    baseline (full local grid + reduce_scatter)."""
     import torch
     wl = W.small(n=20000, n_centers=8192, k=5, nw=3.0, eps=1e-9, seed=3)
-    ss = D.SampleSplit(wl.times, wl.centers, wl.f_max, float(wl.f_w[0]), 5, 1e-9)
+    ss = D.SampleSplit(wl.times, wl.centers, wl.f_max, float(wl.f_w[0]), 5, 1e-9, fused=fused)
+    assert ss.fused == fused
     x = torch.as_tensor(wl.values, device="cuda")
     p = torch.zeros(wl.centers.size, dtype=torch.float64, device="cuda")
     ss.estimate(x, p)
@@ -109,3 +113,48 @@ def test_sample_split_emulated_ranks_on_one_gpu(kern, ranks):
     torch.cuda.synchronize()
     p = power.cpu().numpy() / 7.0
     assert rel_l2(p, p_full) < 1e-12
+
+
+@pytest.mark.parametrize("kern", ["gaussian", "es"])
+@pytest.mark.parametrize("ranks", [2, 3])
+def test_fused_slot_exchange_emulated_ranks_on_one_gpu(kern, ranks):
+    """The fused sample-split exchange with G ranks emulated on one GPU: rank r's spread stores
+    taper k straight into owner k // per's receive slot r (device pointer table; peer NVLink
+    addresses on a multi-GPU box), each owner sums its G slots in rank order and transforms its
+    tapers.  P equals the single-GPU P; K = 7 pads to a multiple of G (empty padding tapers)."""
+    import torch
+    wl = W.c2(n=1 << 18)
+    eng = D.DeviceEngine()
+    full = eng.create(wl.times, wl.centers, wl.f_max, float(wl.f_w[0]), 7, 1e-9, "f64", None)
+    w = full.tapers()[0]
+    p_full = full.power(wl.values)[0]
+    kpad = -(-7 // ranks) * ranks
+    per = kpad // ranks
+    mr = eng.mr(full)
+    parts, rows = [], []
+    for r in range(ranks):
+        s0, s1 = D.split_range(wl.n, ranks, r)
+        e = eng.create(wl.times[s0:s1], wl.centers, wl.f_max, float(wl.f_w[0]), 7, 1e-9, "f64", w[:, s0:s1])
+        parts.append((e, s0, s1))
+        rows.append(eng.grid_rows(e))
+    occ = np.zeros(rows[0][2], dtype=bool)
+    for lo, cnt, nr in rows:
+        occ[(lo + np.arange(cnt)) % nr] = True
+    lo, cnt = D.covering_interval(occ)
+    recv = [torch.zeros((ranks, per, 2 * mr), dtype=torch.float64, device="cuda") for _ in range(ranks)]
+    for r, (e, s0, s1) in enumerate(parts):
+        eng.set_grid_rows(e, lo, cnt)
+        ptrs = torch.tensor([recv[o].data_ptr() + r * per * mr * 16 for o in range(ranks)], dtype=torch.int64,
+                            device="cuda")
+        eng.spread_slots(e, torch.as_tensor(wl.values[s0:s1], device="cuda"), 0, s1 - s0, ptrs, per)
+    power = torch.zeros(wl.centers.size, dtype=torch.float64, device="cuda")
+    for o, (e, _, _) in enumerate(parts):
+        owned = torch.zeros((per, 2 * mr), dtype=torch.float64, device="cuda")
+        eng.sum_slots(recv[o], ranks, per * mr, per * mr, owned)
+        k0, k1 = o * per, min(7, (o + 1) * per)
+        if k1 > k0:
+            pr = torch.zeros_like(power)
+            eng.transform(e, owned, k0, k1, 1.0, pr)
+            power += pr
+    torch.cuda.synchronize()
+    assert rel_l2(power.cpu().numpy() / 7.0, p_full) < 1e-12
