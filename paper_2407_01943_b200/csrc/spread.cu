@@ -360,10 +360,15 @@ __device__ inline void tc_load(TcPoint<Real, G>& q, int ti, const TcCursor& u, i
       P.taper_base + (static_cast<int64_t>(u.c) * P.k_total + P.k0) * P.tstride_k + (u.b0 + j) * P.tstride_j;
   // rows k >= kg re-read row kg - 1 (never staged): the pointer stops advancing there
   const int64_t stride = P.tstride_k;
+  if constexpr (G == 1) {
 #pragma unroll
-  for (int k = 0; k < 8 * G; ++k) {
-    q.w[k] = *tp;
-    if (k + 1 < P.kg) tp += stride;
+    for (int k = 0; k < 8; ++k) {
+      q.w[k] = *tp;
+      if (k + 1 < P.kg) tp += stride;
+    }
+  } else {  // independent addresses: the 16 loads issue back to back
+#pragma unroll
+    for (int k = 0; k < 8 * G; ++k) q.w[k] = tp[min(k, P.kg - 1) * stride];
   }
 }
 
@@ -725,14 +730,26 @@ void spread_typed(const Plan& plan, const SpreadArgs& a, cudaStream_t s) {
   const int ns = p.kernel == NUS_KERNEL_ES ? p.sw : 0;
   const int64_t k = a.tapers ? a.k : 1;
   // 9..16 tapers of a real series: both groups from one staging of the points
-  static const bool two_ok = [] {
+  static const bool two_ok = [] {  // opt-in (NUS_SPREAD_GROUPS=2), see below
     const char* e = std::getenv("NUS_SPREAD_GROUPS");
-    return !(e && std::strcmp(e, "1") == 0);
+    return e && std::strcmp(e, "2") == 0;
   }();
-  if (tc && two_ok && k > 8 && k <= 16 && !a.x_complex) {
-    P.k0 = 0;
-    P.kg = static_cast<int>(k);
-    launch_tc_x<Real>(P, ns, s, true);
+  // Two groups per staging (3 CTAs / SM) measured 476 vs 624 us on C4's structure at 2^22 with
+  // per-cell Horner weights, but with the even/odd weights it is slower than two single-group
+  // launches (C4 646 vs 615 us, C5 K = 15 up to 1.5x): opt-in, and only on dense data (>= 48
+  // points per occupied 32-cell segment).
+  const bool dense = p.n >= 48 * P.nseg_used;
+  if (tc && two_ok && dense && k > 8 && !a.x_complex) {  // launches of <= 16 tapers, balanced
+    const int64_t launches = (k + 15) / 16;
+    int64_t kb = 0;
+    for (int64_t li = 0; li < launches; ++li) {
+      const int64_t kn = (k - kb + (launches - li) - 1) / (launches - li);
+      P.k0 = static_cast<int>(kb);
+      P.kg = static_cast<int>(kn);
+      if (kn > 8) launch_tc_x<Real>(P, ns, s, true);
+      else launch_tc_x<Real>(P, ns, s);
+      kb += kn;
+    }
     return;
   }
   // taper groups of at most 8, balanced
