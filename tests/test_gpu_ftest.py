@@ -4,7 +4,7 @@ import pytest
 
 import paper_2407_01943_b200 as nus
 from paper_2407_01943_b200 import workloads as W
-from conftest import golden, rel_l2
+from conftest import KERNELS, golden, kernel_tol, rel_l2
 from oracle import REF, ref_available
 
 pytestmark = pytest.mark.gpu
@@ -14,7 +14,8 @@ def _c1_plan(g):
     return nus.BandPlan.from_centers(g["centers"], float(g["f_w"]), float(g["f_max"]))
 
 
-def test_f_test_on_reference_tapers_matches_reference_golden():
+@pytest.mark.parametrize("kern", KERNELS)
+def test_f_test_on_reference_tapers_matches_reference_golden(kern):
     g, gf = golden("c1.npz"), golden("ftest_c1.npz")
     grid = nus.SamplingGrid(g["t"])
     plan = _c1_plan(g)
@@ -22,8 +23,9 @@ def test_f_test_on_reference_tapers_matches_reference_golden():
     nplan = nus.NufftPlan(grid, g["centers"], float(g["eps"]))
     j = nus.eigencoefficients(tapers, nus.SignalSeries(grid, g["x"]), nplan)
     r = nus.f_test(j, tapers, plan)
-    assert rel_l2(r.f_stat, gf["f"]) < 1e-9
-    assert rel_l2(r.amplitude, gf["amp"]) < 1e-9
+    tol = kernel_tol(kern, 1e-9, 1e-7)  # ES: a different window within the same eps contract
+    assert rel_l2(r.f_stat, gf["f"]) < tol
+    assert rel_l2(r.amplitude, gf["amp"]) < tol
     assert np.array_equal(r.flags, gf["flags"])
     np.testing.assert_allclose([c for _, c in r.critical_values], gf["crit"], rtol=1e-10)
     assert r.dof == (2, 12)
@@ -31,7 +33,8 @@ def test_f_test_on_reference_tapers_matches_reference_golden():
     assert abs(plan.center(int(np.argmax(r.f_stat))) - 10.0) < 0.1
 
 
-def test_estimator_f_test_with_device_resident_j():
+@pytest.mark.parametrize("kern", KERNELS)
+def test_estimator_f_test_with_device_resident_j(kern):
     g = golden("c1.npz")
     wl = W.c1()
     plan = _c1_plan(g)
@@ -41,7 +44,7 @@ def test_estimator_f_test_with_device_resident_j():
     w = est.tapers().weights_matrix()
     if ref_available():
         f, amp, flags, crit = REF.f_test(wl.times, w, wl.values, wl.centers, wl.eps, wl.f_max, float(wl.f_w[0]))
-        assert rel_l2(r.f_stat, f) < 1e-9 and np.array_equal(r.flags, flags)
+        assert rel_l2(r.f_stat, f) < kernel_tol(kern, 1e-9, 1e-7) and np.array_equal(r.flags, flags)
     # vs the reference's own tapers: F is taper-sign invariant and within the DPSS accuracy
     gf = golden("ftest_c1.npz")
     assert rel_l2(r.f_stat, gf["f"]) < 1e-5

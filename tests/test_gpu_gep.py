@@ -77,7 +77,8 @@ def test_generalized_eigen_errors():
         nus.gpss_exact(nus.SamplingGrid(t), nus.SignalBand(0.5), nus.AnalysisBand(0.45, 0.1), 3)
 
 
-def test_mtnufft0_estimator_matches_reference():
+@pytest.mark.parametrize("kern", ["gaussian", "es"])
+def test_mtnufft0_estimator_matches_reference(kern):
     g = golden("gep_mtnufft0.npz")
     grid = nus.SamplingGrid(g["t"])
     f_w = float(g["f_w"])
