@@ -372,9 +372,14 @@ __device__ inline void tc_load(TcPoint<Real, G>& q, int ti, const TcCursor& u, i
   }
 }
 
+// Unconditional (clamped) load, like the other prefetches: a conditional load with a default
+// value put the default's register write behind the round's just-issued prefetch loads (one
+// instruction held 19 % of the kernel's stall samples on the long scoreboard)
 template <typename Real>
 __device__ inline int tc_perm(const TcCursor& u, int lane, const SpreadParams<Real>& P) {
-  return (u.valid && lane < u.nb) ? P.perm[static_cast<int64_t>(u.c) * P.n + u.b0 + lane] : 0;
+  const int j = lane < u.nb ? lane : 0;
+  const int64_t i = u.valid ? static_cast<int64_t>(u.c) * P.n + min(static_cast<int64_t>(u.b0 + j), P.n - 1) : 0;
+  return P.perm[i];
 }
 
 // ES window polynomials of every even ns (es.cu es_fit), uploaded once per device: with ns a
