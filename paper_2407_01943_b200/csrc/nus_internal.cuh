@@ -242,6 +242,8 @@ struct DpssResult {
 };
 // vectors on device: d_vec [K][n] fp64
 DpssResult dpss_device(int64_t n, double tw, int64_t k, double* d_vec, cudaStream_t s);
+DpssResult dpss_from_coarse(const double* d_diag, const double* d_off, int64_t n, double tw, int64_t k,
+                            double* d_vec, cudaStream_t s);
 DpssResult tridiag_top_device(const double* d_diag, const double* d_off, int64_t n, int64_t k,
                               double* d_vec, cudaStream_t s);
 void dpss_concentrations(int64_t n, double tw, int64_t k, const double* d_vec, double* conc,

@@ -340,6 +340,24 @@ __global__ void __launch_bounds__(kRqThreads) rayleigh_partials_kernel(
   }
 }
 
+// Start vectors for large n from the DPSS of a coarse length nc (same NW): fine index m sits at
+// coarse position u = m (nc - 1) / (n - 1); 4-point Lagrange interpolation (the vectors vary on
+// a scale of ~nc / NW coarse samples, so the interpolant is far below the O(1/nc) difference
+// between the two lengths' sequences, which the inverse iteration removes)
+__global__ void coarse_start_kernel(const double* __restrict__ cv, int64_t nc, int64_t n, int k, dd* __restrict__ xs) {
+  const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (g >= n * k) return;
+  const int64_t j = g / n, m = g - j * n;
+  const double u = static_cast<double>(m) * static_cast<double>(nc - 1) / static_cast<double>(n - 1);
+  int64_t i0 = static_cast<int64_t>(floor(u)) - 1;
+  i0 = i0 < 0 ? 0 : (i0 > nc - 4 ? nc - 4 : i0);
+  const double* v = cv + j * nc + i0;
+  const double x = u - static_cast<double>(i0);  // in [0, 3]
+  const double l0 = -(x - 1.0) * (x - 2.0) * (x - 3.0) / 6.0, l1 = x * (x - 2.0) * (x - 3.0) / 2.0;
+  const double l2 = -x * (x - 1.0) * (x - 3.0) / 2.0, l3 = x * (x - 1.0) * (x - 2.0) / 6.0;
+  xs[g] = dd{l0 * v[0] + l1 * v[1] + l2 * v[2] + l3 * v[3], 0.0};
+}
+
 // out[j][i] = x_j[i] * scale_j  (dd -> fp64)
 __global__ void dd_finalize_kernel(const dd* __restrict__ xs, const double* __restrict__ scales,
                                    int64_t n, int k, double* __restrict__ out) {
@@ -1048,6 +1066,115 @@ DpssResult tridiag_top_device(const double* d_diag, const double* d_off, int64_t
   return res;
 }
 
+namespace {
+
+// Rayleigh quotient shift update sig <- sig + x^T (T - sig) x / x^T x for every row of xs
+void rayleigh_update(const double* d_diag, const double* d_off, int64_t n, int64_t k, const dd* xs,
+                     std::vector<double>& sig_hi, std::vector<double>& sig_lo, cudaStream_t s) {
+  DeviceBuffer d_sh(k * sizeof(double)), d_sl(k * sizeof(double));
+  NUS_CUDA(cudaMemcpyAsync(d_sh.ptr, sig_hi.data(), k * sizeof(double), cudaMemcpyHostToDevice, s));
+  NUS_CUDA(cudaMemcpyAsync(d_sl.ptr, sig_lo.data(), k * sizeof(double), cudaMemcpyHostToDevice, s));
+  const unsigned rb = 296;
+  DeviceBuffer part(static_cast<size_t>(k) * rb * 2 * sizeof(double));
+  rayleigh_partials_kernel<<<dim3(rb, static_cast<unsigned>(k)), kRqThreads, 0, s>>>(
+      d_diag, d_off, n, xs, d_sh.as<double>(), d_sl.as<double>(), part.as<double>());
+  note_launch();
+  check_launch("rayleigh_partials_kernel");
+  std::vector<double> hp(static_cast<size_t>(k) * rb * 2);
+  NUS_CUDA(cudaMemcpyAsync(hp.data(), part.ptr, hp.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+  NUS_CUDA(cudaStreamSynchronize(s));
+  for (int64_t j = 0; j < k; ++j) {
+    long double xr = 0.0L, xx = 0.0L;
+    for (unsigned b = 0; b < rb; ++b) {
+      xr += hp[2 * (j * rb + b)];
+      xx += hp[2 * (j * rb + b) + 1];
+    }
+    const double mu = static_cast<double>(xr / xx);
+    const double s1 = sig_hi[j] + mu, bb = s1 - sig_hi[j];
+    const double err = (sig_hi[j] - (s1 - bb)) + (mu - bb) + sig_lo[j];
+    sig_hi[j] = s1 + err;
+    sig_lo[j] = err - (sig_hi[j] - s1);
+  }
+}
+
+}  // namespace
+
+// DPSS for large n (>= NUS_DPSS_COARSE, default 2^23) without bisection at full length: the DPSS
+// of a coarse length nc = n / 64 (>= 2^17, same NW) interpolated to n gives start vectors within
+// O(1/nc) of the answer; two double-double Rayleigh quotients (against shift 0, then against the
+// first, so the second residual sum carries no N^2-sized cancellation) give shifts within
+// ~(1/nc)^2 x gap of the eigenvalues; then inverse iteration, a refined Rayleigh shift and a
+// second iteration, as the bisection path does after its shifts (C4: 2 full-length solves
+// instead of 5 plus 6 Sturm passes).
+DpssResult dpss_from_coarse(const double* d_diag, const double* d_off, int64_t n, double tw, int64_t k,
+                            double* d_vec, cudaStream_t s) {
+  const bool prof = std::getenv("NUS_DPSS_PROF") != nullptr;
+  auto tic = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!prof) return;
+    NUS_CUDA(cudaStreamSynchronize(s));
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[dpss coarse] %s %.3f s\n", what, std::chrono::duration<double>(now - tic).count());
+    tic = now;
+  };
+  const int64_t nc = std::max<int64_t>(int64_t{1} << 17, n / 64);
+  DeviceBuffer cv(static_cast<size_t>(k) * nc * sizeof(double));
+  dpss_device(nc, tw, k, cv.as<double>(), s);
+  lap("coarse dpss");
+  DeviceBuffer xs(static_cast<size_t>(k) * n * sizeof(dd)), us(static_cast<size_t>(k) * n * 3 * sizeof(dd));
+  coarse_start_kernel<<<blocks_for(n * k, 256), 256, 0, s>>>(cv.as<double>(), nc, n, static_cast<int>(k), xs.as<dd>());
+  note_launch();
+  check_launch("coarse_start_kernel");
+  std::vector<double> sig_hi(k, 0.0), sig_lo(k, 0.0);
+  rayleigh_update(d_diag, d_off, n, k, xs.as<dd>(), sig_hi, sig_lo, s);
+  rayleigh_update(d_diag, d_off, n, k, xs.as<dd>(), sig_hi, sig_lo, s);
+  lap("start vectors + Rayleigh shifts");
+  // ||T|| for the pivot floor (as tridiag_top_device)
+  std::vector<double> hd(n), he(n - 1);
+  NUS_CUDA(cudaMemcpyAsync(hd.data(), d_diag, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  NUS_CUDA(cudaMemcpyAsync(he.data(), d_off, (n - 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
+  NUS_CUDA(cudaStreamSynchronize(s));
+  double anorm = 0.0;
+  for (int64_t i = 0; i < n; ++i)
+    anorm = std::max(anorm, std::fabs(hd[i]) + (i > 0 ? std::fabs(he[i - 1]) : 0.0) + (i + 1 < n ? std::fabs(he[i]) : 0.0));
+  const double pivmin = std::max(anorm, DBL_MIN) * DBL_EPSILON * 1e-3;
+  DeviceBuffer d_sh(k * sizeof(double)), d_sl(k * sizeof(double)), d_norm(2 * k * sizeof(double));
+  for (int pass = 0; pass < 2; ++pass) {
+    NUS_CUDA(cudaMemcpyAsync(d_sh.ptr, sig_hi.data(), k * sizeof(double), cudaMemcpyHostToDevice, s));
+    NUS_CUDA(cudaMemcpyAsync(d_sl.ptr, sig_lo.data(), k * sizeof(double), cudaMemcpyHostToDevice, s));
+    inverse_iteration_dd_warp_kernel<<<static_cast<unsigned>(k), 32, 0, s>>>(
+        d_diag, d_off, n, d_sh.as<double>(), d_sl.as<double>(), 1, pivmin, xs.as<dd>(), us.as<dd>(),
+        d_norm.as<double>());
+    note_launch();
+    check_launch("inverse_iteration_dd_warp_kernel (coarse start)");
+    dd_scale_kernel<<<blocks_for(n * k, 256), 256, 0, s>>>(xs.as<dd>(), d_norm.as<double>(), n, static_cast<int>(k));
+    note_launch();
+    rayleigh_update(d_diag, d_off, n, k, xs.as<dd>(), sig_hi, sig_lo, s);
+    lap(pass == 0 ? "iteration 1 + Rayleigh" : "iteration 2 + Rayleigh");
+  }
+  // xs is normalised (scale 1): finalize with unit scales, then the canonical sign
+  std::vector<double> ones(2 * k);
+  for (int64_t j = 0; j < k; ++j) {
+    ones[2 * j] = 1.0;
+    ones[2 * j + 1] = 0.0;
+  }
+  NUS_CUDA(cudaMemcpyAsync(d_norm.ptr, ones.data(), 2 * k * sizeof(double), cudaMemcpyHostToDevice, s));
+  dd_finalize_kernel<<<blocks_for(n * k, 256), 256, 0, s>>>(xs.as<dd>(), d_norm.as<double>(), n, static_cast<int>(k),
+                                                            d_vec);
+  note_launch();
+  DeviceBuffer sg(k * sizeof(double));
+  absmax_kernel<<<static_cast<unsigned>(k), 1024, 0, s>>>(d_vec, n, sg.as<double>());
+  note_launch();
+  scale_rows_kernel<<<blocks_for(n * k, 256), 256, 0, s>>>(d_vec, n, static_cast<int>(k), sg.as<double>());
+  note_launch();
+  check_launch("dpss finalize");
+  NUS_CUDA(cudaStreamSynchronize(s));
+  DpssResult res;
+  res.values.assign(sig_hi.begin(), sig_hi.end());
+  for (int64_t j = 0; j < k; ++j) res.values[j] += sig_lo[j];
+  return res;
+}
+
 DpssResult dpss_device(int64_t n, double tw, int64_t k, double* d_vec, cudaStream_t s) {
   // tapers.cpp:33-39 validation
   require(n >= 2, "dpss_uniform: n must be >= 2");
@@ -1059,6 +1186,10 @@ DpssResult dpss_device(int64_t n, double tw, int64_t k, double* d_vec, cudaStrea
   dpss_matrix_kernel<<<blocks_for(n, 256), 256, 0, s>>>(n, c, diag.as<double>(), off.as<double>());
   note_launch();
   check_launch("dpss_matrix_kernel");
+  const char* ce = std::getenv("NUS_DPSS_COARSE");
+  const int64_t coarse_from = ce ? std::atoll(ce) : (int64_t{1} << 23);
+  if (n >= coarse_from && n >= 64 && k <= 64)
+    return dpss_from_coarse(diag.as<double>(), off.as<double>(), n, tw, k, d_vec, s);
   return tridiag_top_device(diag.as<double>(), off.as<double>(), n, k, d_vec, s);
 }
 

@@ -165,3 +165,15 @@ def test_dpss_rayleigh_refined_vs_extended_precision_oracle(n, tw, k, force, mon
     tc, ev = C.dpss(n, tw, k)
     assert np.abs(sign_align(d.tapers, tc) - tc).max() < 1e-10
     np.testing.assert_allclose(d.eigenvalues, ev, rtol=1e-13)
+
+
+@pytest.mark.parametrize("n,tw,k", [(1 << 20, 8.0, 15), (1 << 21, 4.0, 7)])
+def test_dpss_from_coarse_start_vs_extended_precision_oracle(n, tw, k, monkeypatch):
+    """Large-n DPSS without full-length bisection (default from 2^23, forced here): the coarse
+    DPSS (n/64, >= 2^17) interpolated to n, double-double Rayleigh shifts, two inverse
+    iterations each followed by a refined shift."""
+    monkeypatch.setenv("NUS_DPSS_COARSE", str(n))
+    d = nus.dpss_uniform(n, tw, k, concentrations=False)
+    tc, ev = C.dpss(n, tw, k)
+    assert np.abs(sign_align(d.tapers, tc) - tc).max() < 1e-10
+    np.testing.assert_allclose(d.eigenvalues, ev, rtol=1e-13)
