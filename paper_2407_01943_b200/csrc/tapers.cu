@@ -1103,9 +1103,9 @@ void rayleigh_update(const double* d_diag, const double* d_off, int64_t n, int64
 // of a coarse length nc = n / 64 (>= 2^17, same NW) interpolated to n gives start vectors within
 // O(1/nc) of the answer; two double-double Rayleigh quotients (against shift 0, then against the
 // first, so the second residual sum carries no N^2-sized cancellation) give shifts within
-// ~(1/nc)^2 x gap of the eigenvalues; then inverse iteration, a refined Rayleigh shift and a
-// second iteration, as the bisection path does after its shifts (C4: 2 full-length solves
-// instead of 5 plus 6 Sturm passes).
+// ~(1/nc)^2 x gap of the eigenvalues; then one double-double inverse iteration and a final
+// Rayleigh quotient (the vectors agree with the bisection path's to 1.8e-16 at 2^23; C4: one
+// full-length solve instead of 5 plus 6 Sturm passes).
 DpssResult dpss_from_coarse(const double* d_diag, const double* d_off, int64_t n, double tw, int64_t k,
                             double* d_vec, cudaStream_t s) {
   const bool prof = std::getenv("NUS_DPSS_PROF") != nullptr;
@@ -1139,7 +1139,9 @@ DpssResult dpss_from_coarse(const double* d_diag, const double* d_off, int64_t n
     anorm = std::max(anorm, std::fabs(hd[i]) + (i > 0 ? std::fabs(he[i - 1]) : 0.0) + (i + 1 < n ? std::fabs(he[i]) : 0.0));
   const double pivmin = std::max(anorm, DBL_MIN) * DBL_EPSILON * 1e-3;
   DeviceBuffer d_sh(k * sizeof(double)), d_sl(k * sizeof(double)), d_norm(2 * k * sizeof(double));
-  for (int pass = 0; pass < 2; ++pass) {
+  const char* pe = std::getenv("NUS_DPSS_COARSE_ITERS");
+  const int passes = pe ? std::max(1, std::atoi(pe)) : 1;  // 1: 1.8e-16 from the bisection path at 2^23
+  for (int pass = 0; pass < passes; ++pass) {
     NUS_CUDA(cudaMemcpyAsync(d_sh.ptr, sig_hi.data(), k * sizeof(double), cudaMemcpyHostToDevice, s));
     NUS_CUDA(cudaMemcpyAsync(d_sl.ptr, sig_lo.data(), k * sizeof(double), cudaMemcpyHostToDevice, s));
     inverse_iteration_dd_warp_kernel<<<static_cast<unsigned>(k), 32, 0, s>>>(
@@ -1150,7 +1152,7 @@ DpssResult dpss_from_coarse(const double* d_diag, const double* d_off, int64_t n
     dd_scale_kernel<<<blocks_for(n * k, 256), 256, 0, s>>>(xs.as<dd>(), d_norm.as<double>(), n, static_cast<int>(k));
     note_launch();
     rayleigh_update(d_diag, d_off, n, k, xs.as<dd>(), sig_hi, sig_lo, s);
-    lap(pass == 0 ? "iteration 1 + Rayleigh" : "iteration 2 + Rayleigh");
+    lap("inverse iteration + Rayleigh");
   }
   // xs is normalised (scale 1): finalize with unit scales, then the canonical sign
   std::vector<double> ones(2 * k);

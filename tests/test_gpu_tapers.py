@@ -170,8 +170,8 @@ def test_dpss_rayleigh_refined_vs_extended_precision_oracle(n, tw, k, force, mon
 @pytest.mark.parametrize("n,tw,k", [(1 << 20, 8.0, 15), (1 << 21, 4.0, 7)])
 def test_dpss_from_coarse_start_vs_extended_precision_oracle(n, tw, k, monkeypatch):
     """Large-n DPSS without full-length bisection (default from 2^23, forced here): the coarse
-    DPSS (n/64, >= 2^17) interpolated to n, double-double Rayleigh shifts, two inverse
-    iterations each followed by a refined shift."""
+    DPSS (n/64, >= 2^17) interpolated to n, double-double Rayleigh shifts, one inverse
+    iteration and a final Rayleigh quotient."""
     monkeypatch.setenv("NUS_DPSS_COARSE", str(n))
     d = nus.dpss_uniform(n, tw, k, concentrations=False)
     tc, ev = C.dpss(n, tw, k)
