@@ -35,6 +35,15 @@ def split_range(n: int, world: int, rank: int):
     return n * rank // world, n * (rank + 1) // world
 
 
+def host_collectives(dist, group=None) -> bool:
+    """gloo (CPU tests, or ranks sharing one GPU): collectives on host tensors and a host
+    barrier after a device synchronise instead of stream-ordered NCCL calls."""
+    try:
+        return dist.is_initialized() and dist.get_backend(group) == "gloo"
+    except Exception:  # pragma: no cover
+        return False
+
+
 def covering_interval(occupied) -> tuple:
     """Smallest cyclic interval (start, length) holding every True of ``occupied``: the
     complement of its longest cyclic run of False (plan.cu's rule for one estimator)."""
@@ -131,15 +140,29 @@ class DeviceEngine:
         C.check(C.lib().nus_sum_slots_device(base.data_ptr(), nslots, slot_stride, count, out.data_ptr(), prec,
                                              self._stream()))
 
-    def ipc_handle(self, t) -> bytes:
+    def ipc_handle(self, t):
+        """(64-byte CUDA IPC handle of the allocation holding t, byte offset of t in it).  The
+        caching allocator may place t inside a larger cudaMalloc segment; torch's own sharing
+        call reports that offset (cudaIpcOpenMemHandle maps the segment base)."""
+        try:
+            info = t.untyped_storage()._share_cuda_()
+            handle, offset = bytes(info[1]), int(info[3]) + t.storage_offset() * t.element_size()
+            if len(handle) == 64:
+                return handle, offset
+        except Exception:  # pragma: no cover - older torch
+            pass
         buf = ctypes.create_string_buffer(64)
         C.check(C.lib().nus_ipc_get_handle(t.data_ptr(), buf))
-        return buf.raw
+        return buf.raw, 0
 
-    def ipc_open(self, handle: bytes) -> int:
+    def ipc_open(self, handle) -> int:
+        raw, offset = handle
         p = ctypes.c_void_p()
-        C.check(C.lib().nus_ipc_open(ctypes.create_string_buffer(handle, 64), self.device, ctypes.byref(p)))
-        return int(p.value)
+        C.check(C.lib().nus_ipc_open(ctypes.create_string_buffer(raw, 64), self.device, ctypes.byref(p)))
+        return int(p.value) + offset
+
+    def synchronize(self):
+        self.torch.cuda.synchronize(self.dev)
 
     def grid_rows(self, est):
         lo, cnt, nr = C._i32(), C._i32(), C._i32()
@@ -218,7 +241,12 @@ class TaperShard:
             power.mul_(float(self.k1 - self.k0))
         else:
             power.zero_()
-        self.dist.reduce(power, dst=0, op=self.dist.ReduceOp.SUM, group=self.group)
+        if host_collectives(self.dist, self.group) and power.is_cuda:
+            host = power.cpu()
+            self.dist.reduce(host, dst=0, op=self.dist.ReduceOp.SUM, group=self.group)
+            power.copy_(host)
+        else:
+            self.dist.reduce(power, dst=0, op=self.dist.ReduceOp.SUM, group=self.group)
         if self.rank == 0:
             power.div_(float(self.k))
         return power
@@ -292,7 +320,7 @@ class SampleSplit:
             return
         occ = torch.zeros(nr, dtype=torch.float64)
         occ[(lo + np.arange(cnt)) % nr] = 1.0
-        if self.engine.__class__.__name__ == "DeviceEngine":
+        if self.engine.__class__.__name__ == "DeviceEngine" and not host_collectives(self.dist, self.group):
             occ = occ.to(self.engine.dev)
         self.dist.all_reduce(occ, op=self.dist.ReduceOp.MAX, group=self.group)
         new_lo, new_cnt = covering_interval(occ.cpu().numpy() > 0)
@@ -308,7 +336,7 @@ class SampleSplit:
             q[k0:k0 + 8] = self.engine.quadform_rows(times, f_max, w[k0:k0 + 8], rows[self.rank],
                                                      rows[self.rank + 1])
         qt = torch.tensor(q, dtype=torch.float64)
-        if self.engine.__class__.__name__ == "DeviceEngine":
+        if self.engine.__class__.__name__ == "DeviceEngine" and not host_collectives(self.dist, self.group):
             qt = qt.to(self.engine.dev)
         self.dist.all_reduce(qt, op=self.dist.ReduceOp.SUM, group=self.group)
         q = qt.cpu().numpy()
@@ -320,8 +348,12 @@ class SampleSplit:
         """x_local: this rank's samples [s1-s0] on the device; rank 0 receives P in ``power``."""
         if self.fused:
             self.engine.spread_slots(self.est, x_local, 0, self.s1 - self.s0, self.slot_ptrs, self.per_rank)
-            if self.world > 1:  # stream-ordered barrier: every rank's slot stores have landed
-                self.dist.all_reduce(self.flag, op=self.dist.ReduceOp.SUM, group=self.group)
+            if self.world > 1:  # every rank's slot stores have landed before any owner sums
+                if host_collectives(self.dist, self.group):
+                    self.engine.synchronize()
+                    self.dist.barrier(group=self.group)
+                else:  # stream-ordered (NCCL)
+                    self.dist.all_reduce(self.flag, op=self.dist.ReduceOp.SUM, group=self.group)
             count = self.per_rank * self.mr
             self.engine.sum_slots(self.recv, self.world, count, count, self.owned)
         else:
@@ -333,7 +365,12 @@ class SampleSplit:
             self.engine.transform(self.est, self.owned, k0, k1, 1.0, power)
         else:
             power.zero_()
-        self.dist.reduce(power, dst=0, op=self.dist.ReduceOp.SUM, group=self.group)
+        if host_collectives(self.dist, self.group) and power.is_cuda:
+            host = power.cpu()
+            self.dist.reduce(host, dst=0, op=self.dist.ReduceOp.SUM, group=self.group)
+            power.copy_(host)
+        else:
+            self.dist.reduce(power, dst=0, op=self.dist.ReduceOp.SUM, group=self.group)
         if self.rank == 0:
             power.div_(float(self.k))
         return power

@@ -125,6 +125,11 @@ class SlotEngine(NumpyEngine):
         self.tmpdir, self.rank = tmpdir, rank
         self.maps = {}  # base address -> float64 array (flat)
 
+    def synchronize(self):
+        for arr in self.maps.values():
+            if isinstance(arr, np.memmap):
+                arr.flush()
+
     def _register(self, arr):
         base = (len(self.maps) + 1) << 40
         self.maps[base] = arr
@@ -141,11 +146,12 @@ class SlotEngine(NumpyEngine):
 
     def ipc_handle(self, t):
         path = os.path.join(self.tmpdir, f"recv{self.rank}.bin").encode()
-        return path + b"\0" * (64 - len(path))
+        return path + b"\0" * (64 - len(path)), 0
 
     def ipc_open(self, handle):
-        path = handle.rstrip(b"\0").decode()
-        return self._register(np.memmap(path, dtype=np.float64, mode="r+").reshape(-1))
+        raw, offset = handle
+        path = raw.rstrip(b"\0").decode()
+        return self._register(np.memmap(path, dtype=np.float64, mode="r+").reshape(-1)) + offset
 
     def _resolve(self, ptr):
         if self.own[0].data_ptr() <= ptr < self.own[0].data_ptr() + self.own[0].numel() * 8:

@@ -158,3 +158,63 @@ def test_fused_slot_exchange_emulated_ranks_on_one_gpu(kern, ranks):
             power += pr
     torch.cuda.synchronize()
     assert rel_l2(power.cpu().numpy() / 7.0, p_full) < 1e-12
+
+
+def _ipc_worker(rank, world, port, q, tapers, kern):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2407_01943_b200 as nus
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    try:
+        torch.cuda.set_device(0)
+        nus.set_spread_kernel(kern)  # the parent's window (the comparison is bit-level)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        wl = W.c2(n=1 << 18)
+        ss = D.SampleSplit(wl.times, wl.centers, wl.f_max, float(wl.f_w[0]), 7, 1e-9, tapers=tapers, fused=True)
+        assert ss.fused and len(ss.peers) == world - 1
+        x = torch.as_tensor(wl.values[ss.s0:ss.s1], device="cuda")
+        p = torch.zeros(wl.centers.size, dtype=torch.float64, device="cuda")
+        ss.estimate(x, p)
+        p2 = torch.zeros_like(p)
+        ss.estimate(x, p2)  # a second spectrum through the same slots
+        if rank == 0:
+            q.put((p.cpu().numpy(), p2.cpu().numpy()))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:  # surface worker failures instead of waiting for the timeout
+        q.put(e)
+        raise
+
+
+@pytest.mark.parametrize("kern", ["gaussian", "es"])
+def test_fused_exchange_real_cuda_ipc_two_processes_one_gpu(kern):
+    """The fused exchange with real CUDA IPC: two processes on one GPU (gloo for the host-side
+    barrier and the small collectives; no kernel waits on another process), each spreading its
+    half of the samples straight into both owners' receive slots through the peer mappings
+    (handle + allocation offset exchanged with all_gather_object).  P equals the single-GPU P."""
+    import multiprocessing as mp
+
+    from paper_2407_01943_b200.api import _Estimator
+    wl = W.c2(n=1 << 18)
+    full = _Estimator(wl.times, wl.centers, wl.f_max, float(wl.f_w[0]), 7, 1e-9, 1, "f64", 0)
+    tapers = full.tapers()[0]
+    p_full = full.power(wl.values)[0]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q, tapers, kern)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+    if isinstance(res, Exception):
+        raise res
+    assert all(p.exitcode == 0 for p in procs)
+    p1, p2 = res
+    assert rel_l2(p1, p_full) < 1e-12
+    assert np.array_equal(p1, p2)
