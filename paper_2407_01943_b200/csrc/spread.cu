@@ -218,7 +218,8 @@ __global__ void __launch_bounds__(kThreads, 5) spread_gather_kernel(const Spread
 // point is a far sentinel; points 32..35 absorb the last 4-point step's overrun.
 constexpr int kTcWarps = 3;       // warps per CTA (each an independent worker)
 constexpr int kTcRows = 36;       // row stride of the private tables (= 4 mod 16)
-constexpr int kTcPts = 35;        // staged point rows: 32 + the last step's overrun (p <= 34)
+constexpr int kTcPts = 32;        // staged point rows; the last step's overrun rows (p <= 34) read
+                                  // row 31 and are masked by their sentinel rel
 constexpr int kTcCtasPerSm = 5;
 
 __device__ inline void dmma_8x8x4(double& d0, double& d1, double a, double b) {
@@ -391,7 +392,7 @@ __constant__ double c_es[kEsTableSize];
 // G taper groups of 8 share one staging of the points (K = 9..16 with G = 2: Z rows 8 G,
 // accumulators per group; 3 CTAs / SM instead of 5)
 template <typename Real, int XK, int NS, int G = 1>
-__global__ void __launch_bounds__(kTcWarps * 32, G == 1 ? kTcCtasPerSm : 3) spread_tc_kernel(const SpreadParams<Real> P) {
+__global__ void __launch_bounds__(kTcWarps * 32, G == 1 ? kTcCtasPerSm : 4) spread_tc_kernel(const SpreadParams<Real> P) {
   using R2 = typename Vec2<Real>::T;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int RS = kTcRows;
@@ -506,7 +507,7 @@ __global__ void __launch_bounds__(kTcWarps * 32, G == 1 ? kTcCtasPerSm : 3) spre
     perm_next = tc_perm(n2, lane, P);
     // ---- per block: its point range by ballot (rel ascends over the lanes), then exact
     // 4-point steps on the tensor cores; a = W(cell - rel) masked to the support
-    const double* wrow = sw + t * RS + g;      // + p0*RS (points p0 + t) + 8b (slot of cell 8b + g)
+    const double* wrow = sw + g;               // + min(p0 + t, 31)*RS (point row) + 8b (slot of cell 8b + g)
     const double2* zcol = sz + g * RS + t;     // + p0
     const int* rcol = srel + t;
 #pragma unroll
@@ -515,7 +516,7 @@ __global__ void __launch_bounds__(kTcWarps * 32, G == 1 ? kTcCtasPerSm : 3) spre
       const int hi = __popc(__ballot_sync(0xffffffffu, rel < 8 * b + 8));
       for (int p0 = lo; p0 < hi; p0 += 4) {  // rows up to hi + 3 <= 34: absent ones are masked
         const int pp = 8 * b + g - rcol[p0];
-        const double wv = wrow[p0 * RS + 8 * b];
+        const double wv = wrow[min(p0 + t, kTcPts - 1) * RS + 8 * b];
         const double a = static_cast<unsigned>(pp) < static_cast<unsigned>(w2) ? wv : 0.0;
 #pragma unroll
         for (int gg = 0; gg < G; ++gg) {  // taper group gg: Z rows 8 gg .. 8 gg + 7
@@ -735,14 +736,14 @@ void spread_typed(const Plan& plan, const SpreadArgs& a, cudaStream_t s) {
   const int ns = p.kernel == NUS_KERNEL_ES ? p.sw : 0;
   const int64_t k = a.tapers ? a.k : 1;
   // 9..16 tapers of a real series: both groups from one staging of the points
-  static const bool two_ok = [] {  // opt-in (NUS_SPREAD_GROUPS=2), see below
+  static const bool two_ok = [] {  // NUS_SPREAD_GROUPS=1 turns it off, see below
     const char* e = std::getenv("NUS_SPREAD_GROUPS");
-    return e && std::strcmp(e, "2") == 0;
+    return !(e && std::strcmp(e, "1") == 0);
   }();
-  // Two groups per staging (3 CTAs / SM) measured 476 vs 624 us on C4's structure at 2^22 with
-  // per-cell Horner weights, but with the even/odd weights it is slower than two single-group
-  // launches (C4 646 vs 615 us, C5 K = 15 up to 1.5x): opt-in, and only on dense data (>= 48
-  // points per occupied 32-cell segment).
+  // Two groups per staging (4 CTAs / SM with 32-row weight tables): on dense data (C4's
+  // clustered windows, ~64 points per 32-cell segment) 543 vs 623 us for two single-group
+  // launches at 2^22; at ~1 point per cell (C5, K = 15) a 3-CTA version was up to 1.5x slower,
+  // so two groups are used from 48 points per occupied segment.
   const bool dense = p.n >= 48 * P.nseg_used;
   if (tc && two_ok && dense && k > 8 && !a.x_complex) {  // launches of <= 16 tapers, balanced
     const int64_t launches = (k + 15) / 16;
