@@ -740,11 +740,15 @@ void spread_typed(const Plan& plan, const SpreadArgs& a, cudaStream_t s) {
     const char* e = std::getenv("NUS_SPREAD_GROUPS");
     return !(e && std::strcmp(e, "1") == 0);
   }();
-  // Two groups per staging (4 CTAs / SM with 32-row weight tables): on dense data (C4's
-  // clustered windows, ~64 points per 32-cell segment) 543 vs 623 us for two single-group
-  // launches at 2^22; at ~1 point per cell (C5, K = 15) a 3-CTA version was up to 1.5x slower,
-  // so two groups are used from 48 points per occupied segment.
-  const bool dense = p.n >= 48 * P.nseg_used;
+  // Two groups per staging (4 CTAs / SM with 32-row weight tables) against two single-group
+  // launches: C3 (fp32, K = 9, ns = 6) 781 vs 1085 us, C4's structure (dense) 543 vs 623 us,
+  // C5 (K = 15 / 31, fp64, ns >= 8) 4-8 % faster; slower only with the narrowest window (ns = 4,
+  // eps >= 1e-4: up to 18 % in fp32 on C5), which keeps single groups unless the data is dense.
+  static const int64_t dense_min = [] {
+    const char* e = std::getenv("NUS_SPREAD_DENSE_MIN");
+    return e ? static_cast<int64_t>(std::atoll(e)) : int64_t{48};
+  }();
+  const bool dense = p.n >= dense_min * P.nseg_used || p.sw >= 6;
   if (tc && two_ok && dense && k > 8 && !a.x_complex) {  // launches of <= 16 tapers, balanced
     const int64_t launches = (k + 15) / 16;
     int64_t kb = 0;
