@@ -298,7 +298,9 @@ def main():
     # ---- e2e through the host C-ABI with pinned buffers: nus_mtnufft_estimate_batch moves every
     # step's own input in (H2D) and its own P out (D2H) inside the timed region; the copies of one
     # step overlap the compute of its neighbours (the same rotation of 4 series as the device leg)
-    e2e_steps = args.e2e_steps or max(3, min(args.steps, 50))
+    # up to 100 steps (pipeline fill / drain amortised), host buffers capped at ~2 GB
+    step_bytes = C_ * (n + nc) * 8
+    e2e_steps = args.e2e_steps or max(3, min(args.steps, 100, int(2e9 // step_bytes)))
     xh = torch.empty((e2e_steps, C_, n), dtype=torch.float64, pin_memory=True).numpy()
     for i in range(e2e_steps):
         xh[i] = np.roll(vals, 17 * (i % nrot), axis=1)
