@@ -1099,7 +1099,7 @@ void rayleigh_update(const double* d_diag, const double* d_off, int64_t n, int64
 
 }  // namespace
 
-// DPSS for large n (>= NUS_DPSS_COARSE, default 2^23) without bisection at full length: the DPSS
+// DPSS for large n (>= NUS_DPSS_COARSE, default 2^20) without bisection at full length: the DPSS
 // of a coarse length nc = n / 64 (>= 2^17, same NW) interpolated to n gives start vectors within
 // O(1/nc) of the answer; two double-double Rayleigh quotients (against shift 0, then against the
 // first, so the second residual sum carries no N^2-sized cancellation) give shifts within
@@ -1189,7 +1189,7 @@ DpssResult dpss_device(int64_t n, double tw, int64_t k, double* d_vec, cudaStrea
   note_launch();
   check_launch("dpss_matrix_kernel");
   const char* ce = std::getenv("NUS_DPSS_COARSE");
-  const int64_t coarse_from = ce ? std::atoll(ce) : (int64_t{1} << 23);
+  const int64_t coarse_from = ce ? std::atoll(ce) : (int64_t{1} << 20);
   if (n >= coarse_from && n >= 64 && k <= 64)
     return dpss_from_coarse(diag.as<double>(), off.as<double>(), n, tw, k, d_vec, s);
   return tridiag_top_device(diag.as<double>(), off.as<double>(), n, k, d_vec, s);
