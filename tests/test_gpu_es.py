@@ -148,3 +148,36 @@ def test_dense_clusters_wrapping_into_empty_first_segment(kern, ncl, n):
     else:
         sub = np.arange(0, c.size, 5)
         assert np.abs(got[sub] - C.ndft_direct(t, y, c[sub])).max() <= 1e-6 * np.abs(y).sum()
+
+
+@pytest.mark.parametrize("kern", ["gaussian", "es"])
+def test_random_problems_meet_the_eps_contract(kern):
+    """30 seeded random problems across the plan's regimes (Mr from 4096 to 2^17: the cuFFT and
+    the fused paths; uniform / jittered / clustered / Poisson times; wraps from < 1 to ~20;
+    complex y; eps from 1e-2 to 1e-12): max|fast - direct| <= eps ||y||_1 (test_nufft.cpp:81-96)."""
+    rng = np.random.default_rng(2407)
+    for case in range(30):
+        n = int(rng.integers(200, 6000))
+        nc = int(2 ** rng.integers(7, 16))
+        eps = float(10 ** -rng.uniform(2, 12))
+        kind = case % 4
+        if kind == 0:
+            t = np.sort(rng.uniform(0, 100, n))
+        elif kind == 1:
+            t = np.arange(n) + rng.uniform(-0.4, 0.4, n)
+        elif kind == 2:
+            t = np.sort(np.concatenate([c + rng.uniform(0, 0.2, n // 10) for c in rng.uniform(0, 50, 10)]))
+        else:
+            t = np.cumsum(rng.exponential(1.0, n))
+        t = np.unique(t)
+        span = t[-1] - t[0]
+        df = rng.uniform(0.05, 20.0) / span  # 0.05 .. 20 wraps of the grid period
+        c = rng.uniform(-5, 5) * df + df * np.arange(nc)
+        y = rng.standard_normal(t.size) + 1j * rng.standard_normal(t.size)
+        plan = nus.NufftPlan(nus.SamplingGrid(t), c, eps, FAST)
+        got = plan.execute(y)
+        d = C.ndft_direct(t, y, c)
+        err = np.abs(got - d).max() / np.abs(y).sum()
+        # fp64 phases 2 pi f t carry ~1e-16 relative rounding in both sums: the contract's floor
+        floor = 4e-16 * 2 * np.pi * np.abs(c).max() * np.abs(t).max()
+        assert err <= max(eps, floor), (case, n, nc, eps, kind, err, floor)
