@@ -1140,7 +1140,7 @@ DpssResult dpss_from_coarse(const double* d_diag, const double* d_off, int64_t n
   const double pivmin = std::max(anorm, DBL_MIN) * DBL_EPSILON * 1e-3;
   DeviceBuffer d_sh(k * sizeof(double)), d_sl(k * sizeof(double)), d_norm(2 * k * sizeof(double));
   const char* pe = std::getenv("NUS_DPSS_COARSE_ITERS");
-  const int passes = pe ? std::max(1, std::atoi(pe)) : 1;  // 1: 1.8e-16 from the bisection path at 2^23
+  const int passes = pe ? std::max(1, std::atoi(pe)) : 1;  // 1: 1.8e-16 from the bisection path at 2^23 (0: 5e-3)
   for (int pass = 0; pass < passes; ++pass) {
     NUS_CUDA(cudaMemcpyAsync(d_sh.ptr, sig_hi.data(), k * sizeof(double), cudaMemcpyHostToDevice, s));
     NUS_CUDA(cudaMemcpyAsync(d_sl.ptr, sig_lo.data(), k * sizeof(double), cudaMemcpyHostToDevice, s));
