@@ -218,8 +218,9 @@ __global__ void __launch_bounds__(kThreads, 5) spread_gather_kernel(const Spread
 // point is a far sentinel; points 32..35 absorb the last 4-point step's overrun.
 constexpr int kTcWarps = 3;       // warps per CTA (each an independent worker)
 constexpr int kTcRows = 36;       // row stride of the private tables (= 4 mod 16)
-constexpr int kTcPts = 32;        // staged point rows; the last step's overrun rows (p <= 34) read
-                                  // row 31 and are masked by their sentinel rel
+// staged point rows: 32 + the last 4-point step's overrun (p <= 34); with two taper groups the
+// overrun rows read row 31 instead (masked by their sentinel rel), so 4 CTAs/SM fit
+__host__ __device__ constexpr int tc_pts(int groups) { return groups == 1 ? 35 : 32; }
 constexpr int kTcCtasPerSm = 5;
 
 __device__ inline void dmma_8x8x4(double& d0, double& d1, double a, double b) {
@@ -396,13 +397,14 @@ __global__ void __launch_bounds__(kTcWarps * 32, G == 1 ? kTcCtasPerSm : 4) spre
   using R2 = typename Vec2<Real>::T;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int RS = kTcRows;
-  constexpr size_t kWarpBytes = (8 * G * RS) * sizeof(double2) + (kTcPts * RS) * sizeof(double) + RS * sizeof(int);
+  constexpr int PTS = tc_pts(G);
+  constexpr size_t kWarpBytes = (8 * G * RS) * sizeof(double2) + (PTS * RS) * sizeof(double) + RS * sizeof(int);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   double* scq = reinterpret_cast<double*>(smem_raw);     // C_p
   unsigned char* mine = smem_raw + kMaxW2 * sizeof(double) + warp * kWarpBytes;
   double2* sz = reinterpret_cast<double2*>(mine);        // Z [8 tapers][RS points] (rows >= KG stay 0)
-  double* sw = reinterpret_cast<double*>(sz + 8 * G * RS);  // W [kTcPts points][RS], slot = cell mod 32
-  int* srel = reinterpret_cast<int*>(sw + kTcPts * RS);  // rel [RS points]
+  double* sw = reinterpret_cast<double*>(sz + 8 * G * RS);  // W [PTS points][RS], slot = cell mod 32
+  int* srel = reinterpret_cast<int*>(sw + PTS * RS);  // rel [RS points]
 
   const int w2 = NS > 0 ? NS : P.w2;
   if constexpr (NS == 0)
@@ -516,7 +518,7 @@ __global__ void __launch_bounds__(kTcWarps * 32, G == 1 ? kTcCtasPerSm : 4) spre
       const int hi = __popc(__ballot_sync(0xffffffffu, rel < 8 * b + 8));
       for (int p0 = lo; p0 < hi; p0 += 4) {  // rows up to hi + 3 <= 34: absent ones are masked
         const int pp = 8 * b + g - rcol[p0];
-        const double wv = wrow[min(p0 + t, kTcPts - 1) * RS + 8 * b];
+        const double wv = wrow[(PTS > 32 ? p0 + t : min(p0 + t, PTS - 1)) * RS + 8 * b];
         const double a = static_cast<unsigned>(pp) < static_cast<unsigned>(w2) ? wv : 0.0;
 #pragma unroll
         for (int gg = 0; gg < G; ++gg) {  // taper group gg: Z rows 8 gg .. 8 gg + 7
@@ -572,7 +574,7 @@ void es_upload() {  // once per device
 template <typename Real, int XK, int NS, int G = 1>
 void launch_tc(const SpreadParams<Real>& P, cudaStream_t s) {
   const size_t warp_bytes =
-      (8 * G * kTcRows) * sizeof(double2) + (kTcPts * kTcRows) * sizeof(double) + kTcRows * sizeof(int);
+      (8 * G * kTcRows) * sizeof(double2) + (tc_pts(G) * kTcRows) * sizeof(double) + kTcRows * sizeof(int);
   const size_t smem = kMaxW2 * sizeof(double) + kTcWarps * warp_bytes;
   static int blocks_per_sm = 0, sms = 0;
   if (blocks_per_sm == 0) {
