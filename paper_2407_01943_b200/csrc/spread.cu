@@ -393,7 +393,7 @@ __constant__ double c_es[kEsTableSize];
 // G taper groups of 8 share one staging of the points (K = 9..16 with G = 2: Z rows 8 G,
 // accumulators per group; 3 CTAs / SM instead of 5)
 template <typename Real, int XK, int NS, int G = 1>
-__global__ void __launch_bounds__(kTcWarps * 32, G == 1 ? kTcCtasPerSm : 4) spread_tc_kernel(const SpreadParams<Real> P) {
+__global__ void __launch_bounds__(kTcWarps * 32, G == 1 ? (sizeof(Real) == 8 ? 4 : kTcCtasPerSm) : 4) spread_tc_kernel(const SpreadParams<Real> P) {
   using R2 = typename Vec2<Real>::T;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int RS = kTcRows;
@@ -421,17 +421,27 @@ __global__ void __launch_bounds__(kTcWarps * 32, G == 1 ? kTcCtasPerSm : 4) spre
   tc_step(p0, 0, P);  // normalise (fewer used segments than warps)
   TcPos pp = p0;
   tc_step(pp, stride, P);
-  TcCursor cur, n1, n2;
+  // D2 (fp64, one taper group): loads two rounds ahead (a second prefetched point set, 150
+  // registers at 4 CTAs/SM), perm three rounds ahead: C2 fp64 spread 90.6 -> 88.1 us; in fp32 the
+  // one-round prefetch at 5 CTAs/SM stays faster (73.3 vs 77.5 us)
+  constexpr bool D2 = sizeof(Real) == 8 && G == 1;
+  TcCursor cur, n1, n2, n3;
   int4 pre = tc_range(pp, P);
   tc_settle(cur, p0, tc_range(p0, P), P);
   n1 = cur;
   tc_advance(n1, pre, pp, P, stride);
   n2 = n1;
   tc_advance(n2, pre, pp, P, stride);
-  TcPoint<Real, G> pt;
+  if constexpr (D2) {
+    n3 = n2;
+    tc_advance(n3, pre, pp, P, stride);
+  }
+  TcPoint<Real, G> pt, pt1;
   pt.ti = -1;
+  pt1.ti = -1;
   tc_load<Real, XK, G>(pt, tc_perm(cur, lane, P), cur, lane, P);
-  int perm_next = tc_perm(n1, lane, P);
+  if constexpr (D2) tc_load<Real, XK, G>(pt1, tc_perm(n1, lane, P), n1, lane, P);
+  int perm_next = tc_perm(D2 ? n2 : n1, lane, P);
 
   double cr[G][4][2], ci[G][4][2];
 #pragma unroll
@@ -505,8 +515,14 @@ __global__ void __launch_bounds__(kTcWarps * 32, G == 1 ? kTcCtasPerSm : 4) spre
     }
     __syncwarp();
     // ---- prefetch round n1 (its perm is in hand) and the perm of round n2
-    tc_load<Real, XK, G>(pt, perm_next, n1, lane, P);
-    perm_next = tc_perm(n2, lane, P);
+    if constexpr (D2) {
+      pt = pt1;
+      tc_load<Real, XK, G>(pt1, perm_next, n2, lane, P);
+      perm_next = tc_perm(n3, lane, P);
+    } else {
+      tc_load<Real, XK, G>(pt, perm_next, n1, lane, P);
+      perm_next = tc_perm(n2, lane, P);
+    }
     // ---- per block: its point range by ballot (rel ascends over the lanes), then exact
     // 4-point steps on the tensor cores; a = W(cell - rel) masked to the support
     const double* wrow = sw + g;               // + min(p0 + t, 31)*RS (point row) + 8b (slot of cell 8b + g)
@@ -553,7 +569,12 @@ __global__ void __launch_bounds__(kTcWarps * 32, G == 1 ? kTcCtasPerSm : 4) spre
     __syncwarp();  // private tables are restaged next
     cur = n1;
     n1 = n2;
-    tc_advance(n2, pre, pp, P, stride);
+    if constexpr (D2) {
+      n2 = n3;
+      tc_advance(n3, pre, pp, P, stride);
+    } else {
+      tc_advance(n2, pre, pp, P, stride);
+    }
   }
   if (P.slots) __threadfence_system();  // peer-slot stores ordered before the caller's barrier
 }
