@@ -352,7 +352,9 @@ __global__ void __launch_bounds__(NT, NT == 128 ? (sizeof(Real) == 4 ? 6 : 4) : 
   int f = 0, out0 = 0, step = 1;
   pdl_launch_dependents();
   pdl_wait();  // pass A's output (and, for power, the previous reader of P)
-  for (int kk = 0; kk < k_count; ++kk) {
+  // tapers in reverse: pass A wrote them in order, so the last ones are still in L2 for the
+  // first wave of rows
+  for (int kk = k_count - 1; kk >= 0; --kk) {
     const T2* g = grid + (ch * kpad + kk) * mr + static_cast<int64_t>(k1) * C;
     T2 v[16];
 #pragma unroll
