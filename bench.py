@@ -354,6 +354,8 @@ def main():
         "vs_baseline": None, "dtype": "f32" if f32 else "f64", "data": "synthetic",
         "config": {"workload": describe(wl, args.workload), "N": n, "I": nc, "K": k,
                    "channels_per_gpu": C_, "eps": wl.eps,
+                   "window": ("exponential of semicircle" if est.info.kernel == 1 else "Gaussian (the reference's)")
+                             + f", {int(est.info.support)} cells per sample",
                    "parallelism": f"{world} GPU(s), independent series per GPU (no data-path collective)",
                    "l2": "inputs larger than L2: per-step grid K*Mr complex + tables exceed 126 MB; x rotated over 4 resident series"},
         "spectra_per_s": world * C_ * args.steps / (ms_max / 1e3),
