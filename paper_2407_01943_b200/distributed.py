@@ -87,6 +87,7 @@ class DeviceEngine:
         import torch
         self.torch = torch
         self.dev = torch.device("cuda", device)
+        self._mapped = {}  # peer pointer (with allocation offset) -> mapped base, for nus_ipc_close
 
     # taper setup -------------------------------------------------------------
     def taper_spline(self, times, f_max, f_w, k):
@@ -159,7 +160,13 @@ class DeviceEngine:
         raw, offset = handle
         p = ctypes.c_void_p()
         C.check(C.lib().nus_ipc_open(ctypes.create_string_buffer(raw, 64), self.device, ctypes.byref(p)))
+        self._mapped[int(p.value) + offset] = int(p.value)
         return int(p.value) + offset
+
+    def ipc_close(self, ptr: int) -> None:
+        base = self._mapped.pop(ptr, None)
+        if base is not None:
+            C.check(C.lib().nus_ipc_close(ctypes.c_void_p(base)))
 
     def synchronize(self):
         self.torch.cuda.synchronize(self.dev)
@@ -309,6 +316,15 @@ class SampleSplit:
         ptrs = [b + r * per * mr * csize for b in bases]
         self.slot_ptrs = torch.tensor(ptrs, dtype=torch.int64, device=self.recv.device)
         self.flag = torch.zeros(1, dtype=self.real, device=self.recv.device)
+
+    def close(self):
+        """Unmap the peer receive slots (CUDA IPC); the estimator's buffers go with the object."""
+        if getattr(self, "peers", None) and hasattr(self.engine, "ipc_close"):
+            if self.world > 1 and self.dist.is_initialized():
+                self.dist.barrier(group=self.group)  # no rank still writes into a peer's slots
+            for ptr in self.peers.values():
+                self.engine.ipc_close(ptr)
+            self.peers = {}
 
     def _widen_rows(self):
         """Union of the ranks' occupied pass-A rows (a cyclic interval each) -> every rank."""

@@ -180,7 +180,8 @@ def _ipc_worker(rank, world, port, q, tapers, kern):
         ss.estimate(x, p2)  # a second spectrum through the same slots
         if rank == 0:
             q.put((p.cpu().numpy(), p2.cpu().numpy()))
-        dist.barrier()
+        ss.close()  # barrier + unmap the peer slots
+        assert ss.peers == {}
         dist.destroy_process_group()
     except Exception as e:  # surface worker failures instead of waiting for the timeout
         q.put(e)
