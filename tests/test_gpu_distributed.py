@@ -116,25 +116,27 @@ def test_sample_split_emulated_ranks_on_one_gpu(kern, ranks):
 
 
 @pytest.mark.parametrize("kern", ["gaussian", "es"])
-@pytest.mark.parametrize("ranks", [2, 3])
-def test_fused_slot_exchange_emulated_ranks_on_one_gpu(kern, ranks):
+@pytest.mark.parametrize("ranks,cfg", [(2, "c2"), (3, "c2"), (2, "c4"), (3, "c4")])
+def test_fused_slot_exchange_emulated_ranks_on_one_gpu(kern, ranks, cfg):
     """The fused sample-split exchange with G ranks emulated on one GPU: rank r's spread stores
     taper k straight into owner k // per's receive slot r (device pointer table; peer NVLink
     addresses on a multi-GPU box), each owner sums its G slots in rank order and transforms its
-    tapers.  P equals the single-GPU P; K = 7 pads to a multiple of G (empty padding tapers)."""
+    tapers.  P equals the single-GPU P; K = 7 / 15 pads to a multiple of G (empty padding tapers);
+    C4's structure (K = 15, dense windows) takes the two-taper-group spread into the slots."""
     import torch
-    wl = W.c2(n=1 << 18)
+    wl = W.c2(n=1 << 18) if cfg == "c2" else W.c4(n=1 << 18, n_centers=1 << 16, windows=40)
+    K = wl.k
     eng = D.DeviceEngine()
-    full = eng.create(wl.times, wl.centers, wl.f_max, float(wl.f_w[0]), 7, 1e-9, "f64", None)
+    full = eng.create(wl.times, wl.centers, wl.f_max, float(wl.f_w[0]), K, 1e-9, "f64", None)
     w = full.tapers()[0]
     p_full = full.power(wl.values)[0]
-    kpad = -(-7 // ranks) * ranks
+    kpad = -(-K // ranks) * ranks
     per = kpad // ranks
     mr = eng.mr(full)
     parts, rows = [], []
     for r in range(ranks):
         s0, s1 = D.split_range(wl.n, ranks, r)
-        e = eng.create(wl.times[s0:s1], wl.centers, wl.f_max, float(wl.f_w[0]), 7, 1e-9, "f64", w[:, s0:s1])
+        e = eng.create(wl.times[s0:s1], wl.centers, wl.f_max, float(wl.f_w[0]), K, 1e-9, "f64", w[:, s0:s1])
         parts.append((e, s0, s1))
         rows.append(eng.grid_rows(e))
     occ = np.zeros(rows[0][2], dtype=bool)
@@ -151,13 +153,13 @@ def test_fused_slot_exchange_emulated_ranks_on_one_gpu(kern, ranks):
     for o, (e, _, _) in enumerate(parts):
         owned = torch.zeros((per, 2 * mr), dtype=torch.float64, device="cuda")
         eng.sum_slots(recv[o], ranks, per * mr, per * mr, owned)
-        k0, k1 = o * per, min(7, (o + 1) * per)
+        k0, k1 = o * per, min(K, (o + 1) * per)
         if k1 > k0:
             pr = torch.zeros_like(power)
             eng.transform(e, owned, k0, k1, 1.0, pr)
             power += pr
     torch.cuda.synchronize()
-    assert rel_l2(power.cpu().numpy() / 7.0, p_full) < 1e-12
+    assert rel_l2(power.cpu().numpy() / K, p_full) < 1e-12
 
 
 def _ipc_worker(rank, world, port, q, tapers, kern):
