@@ -5,13 +5,13 @@ ARCH     := -gencode arch=compute_100a,code=sm_100a
 PKG      := paper_2407_01943_b200
 SRC      := $(PKG)/csrc
 LIBDIR   := $(PKG)/lib
-CU_SRCS  := $(SRC)/plan.cu $(SRC)/es.cu $(SRC)/spread.cu $(SRC)/fft.cu $(SRC)/transform.cu $(SRC)/tapers.cu $(SRC)/normalise.cu $(SRC)/mtnufft.cu $(SRC)/ftest.cu $(SRC)/gep.cu $(SRC)/capi.cu
+CU_SRCS  := $(SRC)/plan.cu $(SRC)/es.cu $(SRC)/spread.cu $(SRC)/fft.cu $(SRC)/transform.cu $(SRC)/tapers.cu $(SRC)/normalise.cu $(SRC)/mtnufft.cu $(SRC)/ftest.cu $(SRC)/gep.cu $(SRC)/multi.cu $(SRC)/capi.cu
 CU_OBJS  := $(patsubst $(SRC)/%.cu,build/cu/%.o,$(CU_SRCS))
 NVFLAGS  := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC \
             --expt-relaxed-constexpr -Iinclude -I$(SRC) -Xptxas -warn-spills
 HDRS     := include/nus_c.h $(SRC)/nus_internal.cuh $(SRC)/nus_estimator.cuh
 
-.PHONY: all lib cpp oracle reftests iocheck clean
+.PHONY: all lib cpp oracle reftests iocheck dropin_multi clean
 
 all: lib cpp oracle
 
@@ -35,6 +35,12 @@ $(LIBDIR)/libnuspectral_b200.so: $(HOST_OBJS) $(LIBDIR)/libnus_b200.so
 iocheck: tests/io/libiocheck.so
 tests/io/libiocheck.so: tests/io/io_capi.cpp $(LIBDIR)/libnuspectral_b200.so include/nuspectral/io.hpp
 	$(CXX) $(CXXFLAGS) -shared -o $@ $< -L$(LIBDIR) -lnuspectral_b200 -lnus_b200 \
+	    -Wl,-rpath,'$$ORIGIN/../../$(LIBDIR)'
+
+# The drop-in's multi-GPU extension against the single-device estimator (tests/test_gpu_multi.py)
+dropin_multi: tests/dropin/multi_device
+tests/dropin/multi_device: tests/dropin/multi_device.cpp $(LIBDIR)/libnuspectral_b200.so $(wildcard include/nuspectral/*.hpp)
+	$(CXX) -std=c++20 -O2 -Wall -Iinclude -o $@ $< -L$(LIBDIR) -lnuspectral_b200 -lnus_b200 \
 	    -Wl,-rpath,'$$ORIGIN/../../$(LIBDIR)'
 
 # The reference's own doctest files compiled UNCHANGED against the drop-in headers
@@ -64,7 +70,7 @@ build/cu/%.o: $(SRC)/%.cu $(HDRS)
 
 $(LIBDIR)/libnus_b200.so: $(CU_OBJS)
 	@mkdir -p $(LIBDIR)
-	$(NVCC) $(ARCH) -shared -o $@ $^ -lcufft -lcusolver -lcublas -Xlinker -rpath -Xlinker /usr/local/cuda/lib64
+	$(NVCC) $(ARCH) -shared -o $@ $^ -lcusolver -lcublas -Xlinker -rpath -Xlinker /usr/local/cuda/lib64
 
 oracle:
 	$(MAKE) -s -C oracle all

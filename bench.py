@@ -3,8 +3,8 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c2f32|c3|c5] [--impl ours|reference]
 
-One step = one multitaper spectrum estimate (spread of all K tapers -> cuFFT ->
-deconvolve/crop/eigenspectrum) of one synthetic series of the workload, with
+One step = one multitaper spectrum estimate (spread of all K tapers -> the own two-pass FFT
+with the deconvolve/crop/eigenspectrum fused into its second pass) of one synthetic series of the workload, with
 the inputs already resident in HBM (``value``); ``e2e`` is the same metric
 through the host C-ABI entry point nus_mtnufft_estimate with pinned host
 buffers, so each step includes the H2D copy of x and the D2H copy of P(f).
@@ -78,6 +78,14 @@ def describe(wl, name):
         "c4": f"c4: clustered N=2^{int(np.log2(n))} (400 windows), I=2^{int(np.log2(i))}, K={wl.k} (NW={wl.nw:g}), eps={wl.eps:g}, {wl.precision}, all samples on one GPU (BASELINE C4 is N=2^26, I=2^24)",
     }[name]
     return desc
+
+
+def bench_config(wl, name):
+    """The workload keys both arms print (identical dicts: the driver compares them)."""
+    n = wl.times.shape[-1]
+    return {"workload": describe(wl, name), "N": int(n), "I": int(wl.centers.size), "K": int(wl.k),
+            "channels_per_gpu": int(wl.times.shape[0]) if wl.times.ndim == 2 else 1, "eps": wl.eps,
+            "precision": wl.precision}
 
 
 class ClockSampler:
@@ -198,7 +206,9 @@ def run_reference_arm(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": describe(wl, args.workload), "parallelism": f"{threads} host threads"},
+        "config": bench_config(wl, args.workload),
+        "parallelism": f"{threads} host threads (rank 0 only)",
+        "window": "Gaussian (the reference's own gridding kernel)",
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
                          "sample": f"per step: {threads} threads x one taper NUFFT (N={t.size}, "
                                    f"I={wl.centers.size}) through the reference NufftPlan + "
@@ -352,12 +362,11 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32" if f32 else "f64", "data": "synthetic",
-        "config": {"workload": describe(wl, args.workload), "N": n, "I": nc, "K": k,
-                   "channels_per_gpu": C_, "eps": wl.eps,
-                   "window": ("exponential of semicircle" if est.info.kernel == 1 else "Gaussian (the reference's)")
-                             + f", {int(est.info.support)} cells per sample",
-                   "parallelism": f"{world} GPU(s), independent series per GPU (no data-path collective)",
-                   "l2": "inputs larger than L2: per-step grid K*Mr complex + tables exceed 126 MB; x rotated over 4 resident series"},
+        "config": bench_config(wl, args.workload),
+        "window": ("exponential of semicircle" if est.info.kernel == 1 else "Gaussian (the reference's)")
+                  + f", {int(est.info.support)} cells per sample",
+        "parallelism": f"{world} GPU(s), independent series per GPU (no data-path collective)",
+        "l2": "inputs larger than L2: per-step grid K*Mr complex + tables exceed 126 MB; x rotated over 4 resident series",
         "spectra_per_s": world * C_ * args.steps / (ms_max / 1e3),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(xh[0].nbytes),
                 "d2h_bytes_per_step": int(ph[0].nbytes), "steps": e2e_steps,

@@ -184,8 +184,37 @@ typedef struct {
 
 int nus_mtnufft_create(const nus_mtnufft_config_t* cfg, const double* times, const double* centers,
                        const double* tapers, nus_mtnufft_t* out);
+/* Same with a per-channel taper half-bandwidth f_w [channels] (NULL -> cfg->f_w for all): each
+ * channel's tapers are gpss_interpolated(grid_c, SignalBand(f_max), f_w[c], K) as the reference
+ * builds one MtnufftEstimator per channel (estimators.cpp:91-104). */
+int nus_mtnufft_create_channels(const nus_mtnufft_config_t* cfg, const double* times, const double* centers,
+                                const double* f_w, const double* tapers, nus_mtnufft_t* out);
 int nus_mtnufft_destroy(nus_mtnufft_t est);
 int nus_mtnufft_plan_info(nus_mtnufft_t est, nus_plan_info_t* info);
+/* ---- Multi-GPU MtnufftEstimator in one process ----------------
+ * A device list; one estimator part per device; exchanges over peer memory (NVLink) ordered by
+ * CUDA events.  cfg->device is ignored.  Replaces the serial loops of nufft.cpp:194-227 /
+ * estimators.cpp:106-122 for one series (tapers / samples) or many (channels):
+ *   NUS_SHARD_CHANNELS  channels split over the devices, no exchange;
+ *   NUS_SHARD_TAPERS    one series, tapers split, partial spectra summed on devices[0];
+ *   NUS_SHARD_SAMPLES   one series, contiguous sample chunks; the spread stores every taper's
+ *                       grid straight into its owner device's receive slot (peer stores fused into
+ *                       the spread), owners sum slots in device order and transform their tapers.
+ * Results equal the single-device estimator's to rounding (deterministic order).  A device may be
+ * listed more than once (emulated parts on one GPU). */
+typedef struct nus_mtnufft_multi_s* nus_mtnufft_multi_t;
+enum { NUS_SHARD_CHANNELS = 0, NUS_SHARD_TAPERS = 1, NUS_SHARD_SAMPLES = 2 };
+int nus_mtnufft_multi_create(const nus_mtnufft_config_t* cfg, const int32_t* devices, int32_t n_devices,
+                             int32_t sharding, const double* times, const double* centers, const double* f_w,
+                             const double* tapers, nus_mtnufft_multi_t* out);
+int nus_mtnufft_multi_destroy(nus_mtnufft_multi_t est);
+/* x [channels][n] host -> P [channels][I] host. */
+int nus_mtnufft_multi_estimate(nus_mtnufft_multi_t est, const double* x_host, double* power_host);
+/* Normalised tapers [channels][K][n] (time order). */
+int nus_mtnufft_multi_tapers(nus_mtnufft_multi_t est, double* out_host);
+/* Bytes each spectrum moves between devices (peer slot stores + partial spectra). */
+int nus_mtnufft_multi_peer_bytes(nus_mtnufft_multi_t est, int64_t* bytes);
+
 /* Normalised taper weights [channels][K][n] (fp64, time order). */
 int nus_mtnufft_tapers(nus_mtnufft_t est, double* out_host);
 /* Setup timings in ms: [dpss, spline, normalise, plan(bins+sort+tables), total]. */
@@ -228,6 +257,8 @@ int nus_sum_slots_device(const void* base, int64_t nslots, int64_t slot_stride, 
 /* CUDA IPC for the receive slots: 64-byte handle of a device allocation, and a peer mapping of
  * another process's handle (close with nus_ipc_close). */
 int nus_ipc_get_handle(const void* dev_ptr, void* handle64);
+/* Same, plus the byte offset of dev_ptr inside its allocation (peers add it to the mapped base). */
+int nus_ipc_get_handle_offset(const void* dev_ptr, void* handle64, int64_t* offset);
 int nus_ipc_open(const void* handle64, int32_t device, void** dev_ptr);
 int nus_ipc_close(void* dev_ptr);
 int nus_mtnufft_grid_rows(nus_mtnufft_t est, int32_t* row_lo, int32_t* row_cnt, int32_t* nrows);

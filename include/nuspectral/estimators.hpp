@@ -17,11 +17,14 @@
 #include "nuspectral/tapers.hpp"
 
 struct nus_mtnufft_s;
+struct nus_mtnufft_multi_s;
 
 namespace nuspectral {
 
 enum class EstimatorMethod { mtnufft, mtnufft0, bg_fixed, bg_adaptive, baseline };
 enum class TaperMode { interpolated, exact_nominal };
+// B200 extension (not in the reference): how one estimator spreads over several GPUs.
+enum class Sharding { tapers, samples };
 
 std::string method_name(EstimatorMethod m);
 std::optional<EstimatorMethod> method_from_name(const std::string& name);
@@ -44,6 +47,12 @@ class MtnufftEstimator {
     double epsilon = 1e-8;
     TaperMode taper_mode = TaperMode::interpolated;
     NufftPathPolicy path_policy = NufftPathPolicy::auto_select;
+    // B200 extension (absent from the reference, defaulted so reference code compiles unchanged):
+    // more than one device -> the series is sharded over these GPUs of this process
+    // (nus_mtnufft_multi_*: tapers split, or the sample split with the grid exchange fused into the
+    // spread over peer memory).  Empty or one entry: the current device only.
+    std::vector<int> devices = {};
+    Sharding sharding = Sharding::samples;
   };
 
   MtnufftEstimator(const SamplingGrid& grid, const SignalBand& signal_band, const BandPlan& plan,
@@ -65,6 +74,7 @@ class MtnufftEstimator {
   BandPlan plan_;
   Options opts_;
   std::shared_ptr<nus_mtnufft_s> handle_;
+  std::shared_ptr<nus_mtnufft_multi_s> multi_;  // Options::devices with more than one entry
   TaperSet tapers_;
   mutable std::once_flag plan_once_;
   mutable std::unique_ptr<NufftPlan> nufft_plan_;

@@ -85,6 +85,8 @@ def lib_ref():
         _ref.ref_injected_destroy.argtypes = [ctypes.c_void_p]
         _ref.ref_injected_power.argtypes = [ctypes.c_void_p, _dp, _dp]
         _ref.ref_injected_power_many.argtypes = [ctypes.c_void_p, _dp, _i64, _i, _dp]
+        _ref.ref_injected_power_tapers.argtypes = [ctypes.c_void_p, _dp, _i, _dp]
+        _ref.ref_injected_taper_powers.argtypes = [ctypes.c_void_p, _dp, _i, _dp]
         _ref.ref_default_taper_count.restype = _i64
         _ref.ref_default_taper_count.argtypes = [_d]
     return _ref
@@ -465,7 +467,7 @@ class Injected:
 
     def __init__(self, t, w, c, eps, f_max, f_w, policy=1):
         t, w, c = _arr(t), _arr(np.atleast_2d(w)), _arr(c)
-        self.n, self.nc = t.size, c.size
+        self.n, self.nc, self.k = t.size, c.size, w.shape[0]
         self.h = lib_ref().ref_injected_create(_p(t), _i64(t.size), _p(w), _i64(w.shape[0]), _p(c),
                                                _i64(c.size), _d(eps), _i(policy), _d(f_max), _d(f_w))
         if not self.h:
@@ -475,6 +477,20 @@ class Injected:
         x = _arr(x)
         out = np.empty(self.nc)
         _chk(lib_ref().ref_injected_power(self.h, _p(x), _p(out)))
+        return out
+
+    def power_tapers(self, x, threads):
+        """One series, the K tapers on `threads` host threads; bit-identical to power()."""
+        x = _arr(x)
+        out = np.empty(self.nc)
+        _chk(lib_ref().ref_injected_power_tapers(self.h, _p(x), _i(threads), _p(out)))
+        return out
+
+    def taper_powers(self, x, threads):
+        """|J_k(i)|^2 of every injected taper [K][I] (tapers on `threads` host threads)."""
+        x = _arr(x)
+        out = np.empty((self.k, self.nc))
+        _chk(lib_ref().ref_injected_taper_powers(self.h, _p(x), _i(threads), _p(out)))
         return out
 
     def power_many(self, xs, threads):

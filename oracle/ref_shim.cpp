@@ -367,6 +367,58 @@ int ref_injected_power_many(void* h, const double* x, int64_t count, int threads
   });
 }
 
+// One series, its K tapers spread over `threads` host threads (the plan is immutable and
+// execute() is const, nufft.hpp:28-30): |J_k(i)|^2 per taper into out_k [K][bands].
+int ref_injected_taper_powers(void* h, const double* x, int threads, double* out_k) {
+  return guard([&] {
+    auto* e = static_cast<InjectedEstimator*>(h);
+    const size_t n = e->grid.n_samples(), bands = e->plan.n_centers(), K = e->weights.size();
+    const SignalSeries series(e->grid, vec(x, static_cast<int64_t>(n)));
+    std::atomic<size_t> next{0};
+    std::exception_ptr first;
+    std::atomic<bool> failed{false};
+    auto worker = [&] {
+      for (;;) {
+        const size_t k = next.fetch_add(1);
+        if (k >= K || failed.load()) return;
+        try {
+          std::vector<std::vector<cplx>> one(1, std::vector<cplx>(n));
+          for (size_t i = 0; i < n; ++i) one[0][i] = {e->weights[k][i], 0.0};
+          const TaperSet t(e->grid, AnalysisBand(0.0, e->f_w), e->f_max, std::move(one), {}, true);
+          const EigenCoefficients j = eigencoefficients(t, series, e->plan);
+          const cplx* row = j.row(0);
+          double* dst = out_k + k * bands;
+          for (size_t i = 0; i < bands; ++i) dst[i] = std::norm(row[i]);
+        } catch (...) {
+          if (!failed.exchange(true)) first = std::current_exception();
+        }
+      }
+    };
+    std::vector<std::thread> pool;
+    const int nt = std::max(1, std::min<int>(threads, static_cast<int>(K)));
+    for (int i = 0; i < nt; ++i) pool.emplace_back(worker);
+    for (auto& th : pool) th.join();
+    if (first) std::rethrow_exception(first);
+  });
+}
+
+// P of one series with the tapers on `threads` threads: the per-taper |J_k|^2 summed over k in
+// the serial loop's order (estimators.cpp:113-117), so the result is bit-identical to power().
+int ref_injected_power_tapers(void* h, const double* x, int threads, double* out) {
+  return guard([&] {
+    auto* e = static_cast<InjectedEstimator*>(h);
+    const size_t bands = e->plan.n_centers(), K = e->weights.size();
+    std::vector<double> pk(K * bands);
+    const int rc = ref_injected_taper_powers(h, x, threads, pk.data());
+    if (rc != 0) throw std::runtime_error(g_err);
+    std::vector<double> p(bands, 0.0);
+    for (size_t k = 0; k < K; ++k)
+      for (size_t i = 0; i < bands; ++i) p[i] += pk[k * bands + i];
+    const double kk = static_cast<double>(K);
+    for (size_t i = 0; i < bands; ++i) out[i] = p[i] / kk;
+  });
+}
+
 // ---- inference: harmonic F-test on eigencoefficients ------
 
 int ref_f_test(const double* t, int64_t n, const double* w, int64_t k, const double* x,

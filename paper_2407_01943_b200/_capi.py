@@ -103,6 +103,7 @@ _SIGS = {
     "nus_mtnufft_spread_slots_device": [_vp, _vp, _i32, _i64, _i64, _vp, _i64, _vp],
     "nus_sum_slots_device": [_vp, _i64, _i64, _i64, _vp, _i32, _vp],
     "nus_ipc_get_handle": [_vp, _vp],
+    "nus_ipc_get_handle_offset": [_vp, _vp, _i64p],
     "nus_ipc_open": [_vp, _i32, ctypes.POINTER(_vp)],
     "nus_ipc_close": [_vp],
     "nus_mtnufft_set_grid_rows": [_vp, _i32, _i32],
@@ -124,6 +125,13 @@ _SIGS = {
     "nus_taper_spline": [_dp, _i64, _d, _d, _i64, _i32, _dp],
     "nus_gpss_interpolated": [_dp, _i64, _d, _d, _i64, _i32, _dp],
     "nus_mtnufft_create": [ctypes.POINTER(MtnufftConfig), _dp, _dp, _dp, ctypes.POINTER(_vp)],
+    "nus_mtnufft_create_channels": [ctypes.POINTER(MtnufftConfig), _dp, _dp, _dp, _dp, ctypes.POINTER(_vp)],
+    "nus_mtnufft_multi_create": [ctypes.POINTER(MtnufftConfig), _i32p, _i32, _i32, _dp, _dp, _dp, _dp,
+                                 ctypes.POINTER(_vp)],
+    "nus_mtnufft_multi_destroy": [_vp],
+    "nus_mtnufft_multi_estimate": [_vp, _dp, _dp],
+    "nus_mtnufft_multi_tapers": [_vp, _dp],
+    "nus_mtnufft_multi_peer_bytes": [_vp, _i64p],
     "nus_mtnufft_destroy": [_vp],
     "nus_mtnufft_plan_info": [_vp, ctypes.POINTER(PlanInfo)],
     "nus_mtnufft_tapers": [_vp, _dp],

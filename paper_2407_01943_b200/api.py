@@ -32,7 +32,7 @@ __all__ = [
     "f_test", "f_quantile", "kFtestConditionViolated", "kFtestSaturated",
     "GeneralizedEigenOptions", "generalized_hermitian_eigen", "gpss_exact", "EigenPairs",
     "ConditioningError", "SpectralRangeError", "SpreadKernel", "set_spread_kernel",
-    "get_spread_kernel", "spread_kernel",
+    "get_spread_kernel", "spread_kernel", "Radix2Fft", "MultiDeviceEstimator",
 ]
 
 kBandBoundary = 1  # grid.hpp:10
@@ -262,8 +262,11 @@ class NufftPlan:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
-            C.lib().nus_plan_destroy(h)
             self._h = None
+            try:
+                C.lib().nus_plan_destroy(h)
+            except Exception:  # interpreter shutdown: the module globals may already be gone
+                pass
 
     # accessors (nufft.hpp:41-48)
     def n_samples(self):
@@ -338,6 +341,47 @@ def ndft_direct(grid: SamplingGrid, weighted_values, centers, device: int = 0) -
     C.check(C.lib().nus_ndft_direct(C.dptr(t), t.size, C.dptr(y), C.dptr(c), c.size, device,
                                     C.dptr(out)))
     return out.view(np.complex128)
+
+
+# ---------------------------------------------------------------- fft.hpp
+
+class Radix2Fft:
+    """fft.hpp:12-29: forward X_k = sum_j x_j e^{-2 pi i jk/n}; inverse the conjugate transform
+    without the 1/n scale.  Runs on the device (fft.cu's radix-2 Stockham kernels)."""
+
+    def __init__(self, n: int, device: int = 0):
+        n = int(n)
+        if n <= 0 or (n & (n - 1)) != 0:
+            raise InvalidArgument("Radix2Fft: size must be a power of two")
+        self._n, self._device = n, int(device)
+
+    def size(self) -> int:
+        return self._n
+
+    @staticmethod
+    def is_power_of_two(n: int) -> bool:
+        return n != 0 and (n & (n - 1)) == 0
+
+    @staticmethod
+    def next_power_of_two(n: int) -> int:
+        p = 1
+        while p < n:
+            p <<= 1
+        return p
+
+    def _run(self, data, inverse):
+        z = np.ascontiguousarray(np.asarray(data, np.complex128).reshape(-1)).copy()
+        if z.size != self._n:
+            raise InvalidArgument("Radix2Fft: data length differs from the transform size")
+        C.check(C.lib().nus_fft_inplace(z.view(np.float64).ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                        self._n, int(inverse), self._device))
+        return z
+
+    def forward(self, data) -> np.ndarray:
+        return self._run(data, False)
+
+    def inverse(self, data) -> np.ndarray:
+        return self._run(data, True)
 
 
 # ---------------------------------------------------------------- tapers.hpp
@@ -576,14 +620,21 @@ class _Estimator:
             t = t[None, :]
         self.channels, self.n = t.shape
         c = C.f64(centers).reshape(-1)
-        cfg = C.MtnufftConfig(self.channels, self.n, c.size, int(k), float(f_max), float(f_w),
+        # f_w: one half-bandwidth for every channel, or one per channel (each channel's tapers are
+        # built on its own grid with its own f_w, as one reference estimator per channel would)
+        fw = np.atleast_1d(C.f64(f_w)).reshape(-1)
+        if fw.size not in (1, self.channels):
+            raise InvalidArgument("MtnufftEstimator: f_w must be a scalar or one value per channel")
+        fw = np.ascontiguousarray(np.broadcast_to(fw, (self.channels,)), dtype=np.float64)
+        self.f_w = fw
+        cfg = C.MtnufftConfig(self.channels, self.n, c.size, int(k), float(f_max), float(fw[0]),
                               float(epsilon), int(policy), _prec(precision), int(device), 0)
         tp = None
         if tapers is not None:
             tp = C.f64(tapers).reshape(self.channels, int(k), self.n)
         h = ctypes.c_void_p()
-        C.check(C.lib().nus_mtnufft_create(ctypes.byref(cfg), C.dptr(t), C.dptr(c),
-                                           C.dptr(tp) if tp is not None else None, ctypes.byref(h)))
+        C.check(C.lib().nus_mtnufft_create_channels(ctypes.byref(cfg), C.dptr(t), C.dptr(c), C.dptr(fw),
+                                                    C.dptr(tp) if tp is not None else None, ctypes.byref(h)))
         self.h = h
         self.k = int(k)
         self.nc = c.size
@@ -594,8 +645,17 @@ class _Estimator:
     def __del__(self):
         h = getattr(self, "h", None)
         if h:
-            C.lib().nus_mtnufft_destroy(h)
             self.h = None
+            try:
+                C.lib().nus_mtnufft_destroy(h)
+            except Exception:  # interpreter shutdown: the module globals may already be gone
+                pass
+
+    def stage_kernels(self):
+        """Names of the kernels of the three per-spectrum stages (spread; FFT pass A; pass B + crop)."""
+        buf = ctypes.create_string_buffer(256)
+        C.check(C.lib().nus_mtnufft_stage_kernels(self.h, buf, 256))
+        return buf.value.decode().split(";")
 
     def tapers(self):
         out = np.empty((self.channels, self.k, self.n))
@@ -639,6 +699,60 @@ class _Estimator:
         vals = [ctypes.c_double() for _ in range(4)]
         C.check(C.lib().nus_mtnufft_bytes_model(self.h, x_dtype, *[ctypes.byref(v) for v in vals]))
         return dict(zip(["total", "spread", "fft", "crop"], [v.value for v in vals]))
+
+
+class MultiDeviceEstimator:
+    """MtnufftEstimator over several GPUs of this process (include/nus_c.h nus_mtnufft_multi_*):
+    ``sharding`` "channels" (independent channels, no exchange), "tapers" (one series, tapers
+    split, partial spectra summed on devices[0]) or "samples" (one series, contiguous sample chunks,
+    the spread storing each taper's grid straight into its owner device's slot over peer memory).
+    A device may be listed more than once (emulated parts on one GPU)."""
+
+    SHARDINGS = {"channels": 0, "tapers": 1, "samples": 2}
+
+    def __init__(self, times, centers, f_max, f_w, k, epsilon, devices, sharding="samples", precision="f64",
+                 tapers=None, policy=NufftPathPolicy.auto_select):
+        t = C.f64(times)
+        if t.ndim == 1:
+            t = t[None, :]
+        self.channels, self.n = t.shape
+        c = C.f64(centers).reshape(-1)
+        fw = np.ascontiguousarray(np.broadcast_to(np.atleast_1d(C.f64(f_w)).reshape(-1), (self.channels,)),
+                                  dtype=np.float64)
+        devs = np.ascontiguousarray(devices, dtype=np.int32)
+        cfg = C.MtnufftConfig(self.channels, self.n, c.size, int(k), float(f_max), float(fw[0]), float(epsilon),
+                              int(policy), _prec(precision), int(devs[0]), 0)
+        tp = None if tapers is None else C.f64(tapers).reshape(self.channels, int(k), self.n)
+        h = ctypes.c_void_p()
+        C.check(C.lib().nus_mtnufft_multi_create(ctypes.byref(cfg), devs.ctypes.data_as(C._i32p), devs.size,
+                                                 self.SHARDINGS[sharding], C.dptr(t), C.dptr(c), C.dptr(fw),
+                                                 C.dptr(tp) if tp is not None else None, ctypes.byref(h)))
+        self.h, self.k, self.nc = h, int(k), c.size
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h:
+            self.h = None
+            try:
+                C.lib().nus_mtnufft_multi_destroy(h)
+            except Exception:  # interpreter shutdown
+                pass
+
+    def estimate(self, x) -> np.ndarray:
+        x = C.f64(x).reshape(self.channels, self.n)
+        out = np.empty((self.channels, self.nc))
+        C.check(C.lib().nus_mtnufft_multi_estimate(self.h, C.dptr(x), C.dptr(out)))
+        return out
+
+    def tapers(self) -> np.ndarray:
+        out = np.empty((self.channels, self.k, self.n))
+        C.check(C.lib().nus_mtnufft_multi_tapers(self.h, C.dptr(out)))
+        return out
+
+    def peer_bytes(self) -> int:
+        v = ctypes.c_int64()
+        C.check(C.lib().nus_mtnufft_multi_peer_bytes(self.h, ctypes.byref(v)))
+        return int(v.value)
 
 
 def eigencoefficients(tapers: TaperSet, series: SignalSeries, plan: NufftPlan,
@@ -731,6 +845,10 @@ class MtnufftEstimator:
 
     def transform_info(self):
         return self._est.info
+
+    def stage_kernels(self):
+        """Kernels launched per spectrum: [spread, FFT pass A, pass B + crop/power]."""
+        return self._est.stage_kernels()
 
     def method(self) -> str:
         return self._method

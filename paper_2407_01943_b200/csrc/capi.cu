@@ -16,6 +16,11 @@ struct nus_mtnufft_s {
   std::unique_ptr<nus::Estimator> est;
 };
 
+struct nus_mtnufft_multi_s {
+  nus::MultiPtr m;
+  std::mutex mu;
+};
+
 namespace {
 
 thread_local std::string g_last_error;
@@ -254,14 +259,7 @@ int nus_fft_inplace(double* data_host, int64_t n, int32_t inverse, int32_t devic
     nus::use_device(device);
     nus::DeviceBuffer d(n * 2 * sizeof(double));
     NUS_CUDA(cudaMemcpy(d.ptr, data_host, d.bytes, cudaMemcpyHostToDevice));
-    if (n > 1) {
-      cufftHandle h;
-      NUS_CUFFT(cufftPlan1d(&h, static_cast<int>(n), CUFFT_Z2Z, 1));
-      const cufftResult r = cufftExecZ2Z(h, d.as<cufftDoubleComplex>(), d.as<cufftDoubleComplex>(),
-                                         inverse ? CUFFT_INVERSE : CUFFT_FORWARD);
-      cufftDestroy(h);
-      NUS_CUFFT(r);
-    }
+    nus::fft_generic_inplace(d.ptr, n, 1, true, inverse != 0, 0);  // own kernels (fft.cu)
     NUS_CUDA(cudaMemcpy(data_host, d.ptr, d.bytes, cudaMemcpyDeviceToHost));
   });
 }
@@ -464,16 +462,58 @@ int nus_gpss_interpolated(const double* times, int64_t n, double f_max, double f
 
 int nus_mtnufft_create(const nus_mtnufft_config_t* cfg, const double* times, const double* centers,
                        const double* tapers, nus_mtnufft_t* out) {
+  return nus_mtnufft_create_channels(cfg, times, centers, nullptr, tapers, out);
+}
+
+int nus_mtnufft_create_channels(const nus_mtnufft_config_t* cfg, const double* times, const double* centers,
+                                const double* f_w, const double* tapers, nus_mtnufft_t* out) {
   return guarded([&] {
     nus::require(cfg && out, "nus_mtnufft_create: null argument");
     auto h = new nus_mtnufft_s;
     try {
-      h->est = nus::estimator_create(*cfg, times, centers, tapers);
+      h->est = nus::estimator_create(*cfg, times, centers, tapers, f_w);
     } catch (...) {
       delete h;
       throw;
     }
     *out = h;
+  });
+}
+
+int nus_mtnufft_multi_create(const nus_mtnufft_config_t* cfg, const int32_t* devices, int32_t n_devices,
+                             int32_t sharding, const double* times, const double* centers, const double* f_w,
+                             const double* tapers, nus_mtnufft_multi_t* out) {
+  return guarded([&] {
+    nus::require(cfg && out, "nus_mtnufft_multi_create: null argument");
+    auto h = std::make_unique<nus_mtnufft_multi_s>();
+    h->m = nus::multi_create(*cfg, devices, n_devices, sharding, times, centers, f_w, tapers);
+    *out = h.release();
+  });
+}
+
+int nus_mtnufft_multi_destroy(nus_mtnufft_multi_t est) {
+  return guarded([&] { delete est; });
+}
+
+int nus_mtnufft_multi_estimate(nus_mtnufft_multi_t est, const double* x_host, double* power_host) {
+  return guarded([&] {
+    nus::require(est && x_host && power_host, "multi estimate: null argument");
+    std::lock_guard<std::mutex> lock(est->mu);
+    nus::multi_estimate(*est->m, x_host, power_host);
+  });
+}
+
+int nus_mtnufft_multi_tapers(nus_mtnufft_multi_t est, double* out_host) {
+  return guarded([&] {
+    nus::require(est && out_host, "multi tapers: null argument");
+    nus::multi_tapers(*est->m, out_host);
+  });
+}
+
+int nus_mtnufft_multi_peer_bytes(nus_mtnufft_multi_t est, int64_t* bytes) {
+  return guarded([&] {
+    nus::require(est && bytes, "multi peer bytes: null argument");
+    *bytes = nus::multi_peer_bytes(*est->m);
   });
 }
 
@@ -619,6 +659,28 @@ int nus_ipc_get_handle(const void* dev_ptr, void* handle64) {
   });
 }
 
+int nus_ipc_get_handle_offset(const void* dev_ptr, void* handle64, int64_t* offset) {
+  return guarded([&] {
+    nus::require(dev_ptr && handle64 && offset, "ipc: null argument");
+    cudaIpcMemHandle_t h;
+    NUS_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
+    std::memcpy(handle64, &h, sizeof(h));
+    // cudaIpcOpenMemHandle maps the base of the allocation holding dev_ptr: the peer needs the
+    // byte offset of dev_ptr inside it (a caching allocator sub-allocates large segments)
+    using AddrRange = int (*)(unsigned long long*, size_t*, unsigned long long);
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    NUS_CUDA(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+    nus::require(fn != nullptr && q == cudaDriverEntryPointSuccess, "ipc: cuMemGetAddressRange unavailable");
+    unsigned long long base = 0;
+    size_t size = 0;
+    const unsigned long long p = reinterpret_cast<unsigned long long>(dev_ptr);
+    if (reinterpret_cast<AddrRange>(fn)(&base, &size, p) != 0)
+      nus::fail(NUS_ERR_CUDA, "ipc: cuMemGetAddressRange failed");
+    *offset = static_cast<int64_t>(p - base);
+  });
+}
+
 int nus_ipc_open(const void* handle64, int32_t device, void** dev_ptr) {
   return guarded([&] {
     nus::require(handle64 && dev_ptr, "ipc: null argument");
@@ -717,8 +779,18 @@ int nus_mtnufft_f_test(nus_mtnufft_t est, const double* x_host, double cap, doub
     std::vector<double> w0(C * K * 2);
     nus::taper_zero_frequency(e, w0.data());
     nus::DeviceBuffer f(C * nb * sizeof(double)), a(C * nb * 2 * sizeof(double)), fl(C * nb);
-    nus::ftest_device(j.ptr, f32, K, nb, C, w0.data(), e.cfg.n, e.plan->d_centers.as<double>(), e.cfg.f_w, cap,
-                      f.as<double>(), a.as<double>(), fl.as<uint8_t>(), s);
+    bool uniform_fw = true;
+    for (int64_t c = 1; c < C; ++c) uniform_fw = uniform_fw && e.f_w[c] == e.f_w[0];
+    if (uniform_fw) {
+      nus::ftest_device(j.ptr, f32, K, nb, C, w0.data(), e.cfg.n, e.plan->d_centers.as<double>(), e.f_w[0], cap,
+                        f.as<double>(), a.as<double>(), fl.as<uint8_t>(), s);
+    } else {  // each channel's band-edge flag uses its own half-bandwidth
+      const size_t jb = static_cast<size_t>(K) * nb * 2 * (f32 ? sizeof(float) : sizeof(double));
+      for (int64_t c = 0; c < C; ++c)
+        nus::ftest_device(static_cast<const char*>(j.ptr) + c * jb, f32, K, nb, 1, w0.data() + c * K * 2, e.cfg.n,
+                          e.plan->d_centers.as<double>(), e.f_w[c], cap, f.as<double>() + c * nb,
+                          a.as<double>() + 2 * c * nb, fl.as<uint8_t>() + c * nb, s);
+    }
     NUS_CUDA(cudaMemcpy(f_out, f.ptr, f.bytes, cudaMemcpyDeviceToHost));
     NUS_CUDA(cudaMemcpy(amp_out, a.ptr, a.bytes, cudaMemcpyDeviceToHost));
     NUS_CUDA(cudaMemcpy(flags_out, fl.ptr, fl.bytes, cudaMemcpyDeviceToHost));

@@ -1,5 +1,5 @@
-// Two-pass (four-step) power-of-two FFT of the K oversampled grids with the
-// deconvolve / crop / eigenspectrum reduction fused into the second pass.
+// The uniform FFT of the K oversampled grids (every power-of-two Mr), with the deconvolve /
+// crop / eigenspectrum reduction fused into its last pass.  No library FFT anywhere.
 //
 // Replaces Radix2Fft::forward (src/fft.cpp:39-58) + the crop of
 // src/nufft.cpp:161-164 + the power loop of src/estimators.cpp:113-117.
@@ -7,24 +7,30 @@
 //   Mr = R * C, j = j1 C + j2, k = k1 + R k2:
 //   X[k1 + R k2] = sum_j2 w_C^{j2 k2} [ w_Mr^{j2 k1} sum_j1 x[j1 C + j2] w_R^{j1 k1} ]
 //
-// Pass A (fft_cols_kernel): each CTA loads a block of columns (CW consecutive j2,
-//   all R rows: 64-256 B contiguous per row), runs the length-R FFTs in shared
-//   memory, applies the inter-pass twiddle w_Mr^{j2 k1} (two-level table) and
-//   stores the result in place (row k1).
-// Pass B (fft_rows_crop_kernel): each CTA owns RPC consecutive rows k1 and loops
-//   over the K tapers: length-C FFT in shared memory, then for every output bin
-//   k = k1 + R k2 that the crop keeps (m = (-k) mod Mr in [-I/2, I/2)) it adds
-//   |X|^2 into a per-thread register accumulator; after the last taper it writes
-//   P(i) = d_i^2 * sum_k |X_k|^2 / K.  The transformed grid is never written back.
+// Pass A (fft_cols_blk_kernel; fft_cols_small_kernel for R <= 16): each CTA loads one tile of
+//   columns (CW consecutive j2, all R rows; contiguous in the spread's blocked layout), runs
+//   the length-R FFTs, applies the inter-pass twiddle w_Mr^{j2 k1} (two-level table) and
+//   stores the result out of place in the natural layout (row k1).
+// Pass B (fft_rows_crop_kernel): each CTA owns one row k1 and loops over the K tapers:
+//   length-C FFT in shared memory, then for every output bin k = k1 + R k2 that the crop
+//   keeps (m = (-k) mod Mr in [-I/2, I/2)) it adds |X|^2 into a per-thread register
+//   accumulator; after the last taper it writes P(i) = d_i^2 * sum_k |X_k|^2 / K.  The
+//   transformed grid is never written back.
+//
+// Sizes: 512 <= Mr <= 8192 is pass B alone (R = 1, C = Mr, NT = Mr / 16 threads); 2^14 .. 2^23
+// two passes with C = 2048; 2^24 with C = 4096; 2^25 and 2^26 with C = 8192 (512 threads).
+// Grids below 512 cells or above 2^26 (no config comes near either) use the generic radix-2
+// Stockham kernels (one launch per stage) + crop_power_kernel; those also serve the Radix2Fft
+// drop-in and the DPSS concentration convolution.
 //
 // In-CTA FFTs are Stockham autosort stages in shared memory with radix-16/8/4/2
-// register butterflies; every thread handles 16 elements per stage (CTA = 256
-// threads, 4096 complex elements).  Twiddles come from a per-plan table of
-// e^{-2 pi i m / L} built with sincospi (exact argument).
+// register butterflies; every thread handles 16 elements per stage.  Twiddles come from a
+// per-plan table of e^{-2 pi i m / L} built with sincospi (exact argument).
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 
 #include "nus_internal.cuh"
 
@@ -232,45 +238,6 @@ __device__ inline PassATwiddles<T2> pass_a_twiddles(int64_t j2, int out0, int st
 
 // ---- pass A ----------------------------------------------------------------------------
 
-template <typename Real, int R0>
-__global__ void __launch_bounds__(kFftThreads, 2) fft_cols_kernel(
-    typename C2<Real>::T* __restrict__ grid, int64_t mr, int R, int C, int CW, int64_t row_stride,
-    int rows_per_ch, int kpad, const typename C2<Real>::T* __restrict__ tw_r,
-    const typename C2<Real>::T* __restrict__ tw_hi, const typename C2<Real>::T* __restrict__ tw_lo,
-    int lo_bits) {
-  using T2 = typename C2<Real>::T;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T2* const buf = reinterpret_cast<T2*>(smem_raw);  // [R][CW]
-  const int j2_0 = blockIdx.x * CW;
-  const int64_t ch = blockIdx.y;
-  const int lgR = __ffs(R) - 1, lgCW = __ffs(CW) - 1;
-  int fl, out0l, stl;
-  last_stage_out(threadIdx.x, lgR, lgCW, fl, out0l, stl);
-  const PassATwiddles<T2> tw2 = pass_a_twiddles(j2_0 + fl, out0l, stl, mr, lo_bits, tw_hi, tw_lo);
-  for (int kk = 0; kk < rows_per_ch; ++kk) {
-    T2* g = grid + (ch * kpad + kk) * row_stride;
-    T2 v[16];
-#pragma unroll
-    for (int s = 0; s < 16; ++s) {  // coalesced: consecutive threads take consecutive columns
-      int f, e;
-      stage0_index<R0>(s, lgR, lgCW, f, e);
-      v[s] = g[static_cast<int64_t>(e) * C + j2_0 + f];
-    }
-    int f, out0, step;
-    fft16_regs<R0, false>(v, buf, lgR, lgCW, CW, 1, tw_r, f, out0, step);
-    const int64_t j2 = j2_0 + f;
-    T2 w = cmul(tw2.b_hi, tw2.b_lo);  // inter-pass twiddle w_Mr^{j2 k1}, k1 = out0 + q step
-    const T2 wstep = cmul(tw2.s_hi, tw2.s_lo);
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const int k1 = out0 + q * step;
-      g[static_cast<int64_t>(k1) * C + j2] = cmul(v[q], w);
-      if (q < 15) w = cmul(w, wstep);
-    }
-    __syncthreads();  // buf reused by the next taper
-  }
-}
-
 // Pass A over the blocked grid with register loads: one tile (R rows x CW columns, contiguous,
 // NT * 16 elements) per CTA, several CTAs per SM in flight instead of a persistent bulk-copy
 // pipeline.  Rows outside the occupied interval are zeros and are not read.
@@ -323,6 +290,84 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 4 : NT == 256 ? (sizeof(Real) 
   }
 }
 
+// Pass A for short columns (R = 2..16: Mr = 2^14, 2^15 with C = 2048): a column's R cells fit in
+// one thread's registers, so the length-R DFT runs there with no shared memory.  One blocked tile
+// (R rows x CW columns, contiguous) per CTA, each thread taking columns f = tid, tid + 256, ...;
+// loads and stores are coalesced across the columns.
+template <typename Real, int R>
+__global__ void __launch_bounds__(kFftThreads) fft_cols_small_kernel(
+    const typename C2<Real>::T* __restrict__ grid, typename C2<Real>::T* __restrict__ out, int64_t mr, int C, int CW,
+    int lg_nblk, int k, int kpad, const typename C2<Real>::T* __restrict__ tw_hi,
+    const typename C2<Real>::T* __restrict__ tw_lo, int lo_bits, int row_lo, int row_cnt) {
+  using T2 = typename C2<Real>::T;
+  const int t = blockIdx.x;
+  const int blk = t & ((1 << lg_nblk) - 1), ck = t >> lg_nblk;
+  const int ch = ck / k, kk = ck - ch * k;
+  const T2* src = grid + (static_cast<int64_t>(ch) * kpad + kk) * mr + static_cast<int64_t>(blk) * R * CW;
+  T2* g = out + (static_cast<int64_t>(ch) * kpad + kk) * mr;
+  for (int f = threadIdx.x; f < CW; f += kFftThreads) {
+    T2 v[R];
+#pragma unroll
+    for (int e = 0; e < R; ++e) {
+      const bool occ = static_cast<unsigned>((e - row_lo) & (R - 1)) < static_cast<unsigned>(row_cnt);
+      v[e] = occ ? src[e * CW + f] : T2{Real(0), Real(0)};
+    }
+    dft_reg<R>(v);
+    const int j2 = blk * CW + f;
+    // w_Mr^{j2 k1}, k1 = 0..R-1: base 1, step w_Mr^{j2} (two-level table)
+    const PassATwiddles<T2> tw2 = pass_a_twiddles(static_cast<int64_t>(j2), 0, 1, mr, lo_bits, tw_hi, tw_lo);
+    const T2 wstep = cmul(tw2.s_hi, tw2.s_lo);
+    T2 w = wstep;
+    g[j2] = v[0];
+#pragma unroll
+    for (int k1 = 1; k1 < R; ++k1) {
+      g[static_cast<int64_t>(k1) * C + j2] = cmul(v[k1], w);
+      if (k1 + 1 < R) w = cmul(w, wstep);
+    }
+  }
+}
+
+// ---- generic radix-2 Stockham FFT (any power of two; one launch per stage) ---------------
+// For grids outside the fused passes (Mr < 512, Mr > 2^26), the Radix2Fft drop-in and the DPSS
+// concentration convolution.  Stage with half-span ns: y[2(j - k) + k] = a + w b,
+// y[2(j - k) + k + ns] = a - w b with a = x[j], b = x[j + n/2], k = j mod ns,
+// w = e^{-+ i pi k / ns} (sincospi, exact argument).  Rows r < rows of length n live at
+// ((r / kin) kpad_in + r % kin) n on input and ((r / kin) kpad_out + r % kin) n on output.
+template <typename T2>
+__global__ void stockham_r2_kernel(const T2* __restrict__ x, T2* __restrict__ y, int64_t n, int64_t ns,
+                                   int64_t rows, int64_t kin, int64_t kpad_in, int64_t kpad_out, int inverse) {
+  using Real = decltype(T2{}.x);
+  const int64_t half = n >> 1;
+  const int64_t total = rows * half;
+  for (int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; g < total;
+       g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = g / half, j = g - r * half;
+    const int64_t rc = r / kin, rk = r - rc * kin;
+    const T2* xr = x + (rc * kpad_in + rk) * n;
+    T2* yr = y + (rc * kpad_out + rk) * n;
+    const int64_t k = j & (ns - 1);
+    double sn, cs;
+    sincospi((inverse ? 1.0 : -1.0) * static_cast<double>(k) / static_cast<double>(ns), &sn, &cs);
+    const T2 a = xr[j], b = xr[j + half];
+    const Real c = static_cast<Real>(cs), s = static_cast<Real>(sn);
+    const T2 bw{b.x * c - b.y * s, b.x * s + b.y * c};
+    const int64_t o = ((j - k) << 1) + k;
+    yr[o] = T2{a.x + bw.x, a.y + bw.y};
+    yr[o + ns] = T2{a.x - bw.x, a.y - bw.y};
+  }
+}
+
+template <typename T2>
+__global__ void copy_rows_kernel(const T2* __restrict__ x, T2* __restrict__ y, int64_t n, int64_t rows, int64_t kin,
+                                 int64_t kpad_in, int64_t kpad_out) {
+  for (int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; g < rows * n;
+       g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = g / n, i = g - r * n;
+    const int64_t rc = r / kin, rk = r - rc * kin;
+    y[(rc * kpad_out + rk) * n + i] = x[(rc * kpad_in + rk) * n + i];
+  }
+}
+
 // ---- pass B + crop / power ---------------------------------------------------------------
 
 constexpr int kCropN = 9;  // last-stage outputs q the crop can keep (pass B, Mr >= 2 nc)
@@ -331,8 +376,11 @@ __host__ __device__ constexpr int crop_q(int c) { return c < 5 ? c : c + 7; }
 // NT threads per row: 256 for C = 4096 (2 CTAs / SM), 128 for C = 2048 (4 CTAs / SM, twice the
 // rows in flight to cover the row loads).
 // C = NT * 16 is fixed by NT, so every index of the in-CTA FFT is a compile-time constant
+__host__ __device__ constexpr int lg_threads(int nt) { return nt <= 1 ? 0 : 1 + lg_threads(nt / 2); }
+
+// NT = 32 / 64 (C = 512 / 1024): single-pass transforms of small grids (R = 1), several rows per SM.
 template <typename Real, typename PReal, int R0, int NT = kFftThreads>
-__global__ void __launch_bounds__(NT, NT == 128 ? (sizeof(Real) == 4 ? 6 : 4) : NT == 256 ? (sizeof(Real) == 4 ? 3 : 2) : 1) fft_rows_crop_kernel(
+__global__ void __launch_bounds__(NT, NT <= 64 ? 8 : NT == 128 ? (sizeof(Real) == 4 ? 6 : 4) : NT == 256 ? (sizeof(Real) == 4 ? 3 : 2) : 1) fft_rows_crop_kernel(
     const typename C2<Real>::T* __restrict__ grid, int64_t mr, int R, int C, int RPC, int64_t kpad,
     int k_count, int64_t nc, int64_t mode_offset, const Real* __restrict__ deconv,
     const typename C2<Real>::T* __restrict__ tw_c, typename C2<Real>::T* __restrict__ j_out,
@@ -342,7 +390,7 @@ __global__ void __launch_bounds__(NT, NT == 128 ? (sizeof(Real) == 4 ? 6 : 4) : 
   T2* const buf = reinterpret_cast<T2*>(smem_raw);  // [C] (swizzled)
   const int k1 = blockIdx.x;                        // one row per CTA
   const int64_t ch = blockIdx.y;
-  constexpr int lgC = NT == 128 ? 11 : NT == 256 ? 12 : 13;
+  constexpr int lgC = lg_threads(NT) + 4;  // NT threads x 16 registers
   C = 1 << lgC;
   // Mr >= 2 nc, so the crop keeps k2 <= C/4 or k2 >= 3C/4 only: of this thread's outputs
   // k2 = out0 + q C/16 that is q in {0..4, 12..15} (kCropQ); the other seven are never formed
@@ -727,28 +775,83 @@ bool pdl_enabled() {
 }
 
 bool fused_fft_supported(const PlanParams& p) {
-  // 4096-element in-CTA FFTs need >= 2 stages per pass: C = 4096 rows, R = Mr / 4096 = 1 or >= 32
-  // Mr = 2^25 (C4) runs both passes as 8192-element in-CTA FFTs (512 threads, 128 KB tiles)
-  return p.mr == kFftElems || (p.mr >= (int64_t{1} << 17) && p.mr <= (int64_t{1} << 25));
+  // single pass (R = 1) for 512 <= Mr <= 8192: one C = Mr row per CTA, NT = Mr / 16 threads;
+  // two passes above: C = 2048 up to 2^23 (R = 8 .. 4096), 4096 at 2^24, 8192 at 2^25 / 2^26.
+  // Smaller and larger grids take the generic radix-2 kernels (fft_generic_rows).
+  return p.mr >= 512 && p.mr <= (int64_t{1} << 26);
 }
+
+namespace {
+// Kernel attributes are per device: configured once for every device a process uses.
+void configure_fft_kernels() {
+  static std::mutex mu;
+  static bool done[64] = {};
+  int dev = 0;
+  NUS_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 64 && done[dev]) return;
+  const int smem = kFftElems * static_cast<int>(sizeof(double2));
+#define NUS_ATTR(KERN) NUS_CUDA(cudaFuncSetAttribute(KERN, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))
+  NUS_ATTR((fft_rows_crop_kernel<double, double, 16>));
+  NUS_ATTR((fft_cols_blk_kernel<double, 16, kFftThreads>));
+  NUS_ATTR((fft_cols_blk_kernel<double, 8, kFftThreads>));
+  NUS_ATTR((fft_cols_blk_kernel<double, 4, kFftThreads>));
+  NUS_ATTR((fft_cols_blk_kernel<double, 2, kFftThreads>));
+  NUS_ATTR((fft_cols_blk_kernel<double, 4, kFftThreads, 6>));
+  NUS_ATTR((fft_cols_blk_kernel<double, 8, kFftThreads, 7>));
+  NUS_ATTR((fft_cols_blk_kernel<double, 16, kFftThreads, 8>));
+  NUS_ATTR((fft_cols_blk_kernel<double, 2, kFftThreads, 9>));
+  NUS_ATTR((fft_cols_blk_kernel<double, 4, kFftThreads, 10>));
+  NUS_ATTR((fft_cols_blk_kernel<double, 8, kFftThreads, 11>));
+  NUS_ATTR((fft_cols_blk_kernel<double, 16, kFftThreads, 12>));
+#undef NUS_ATTR
+  const int smem_w = 2 * kFftElems * static_cast<int>(sizeof(double2));
+#define NUS_ATTRW(KERN) NUS_CUDA(cudaFuncSetAttribute(KERN, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_w))
+  NUS_ATTRW((fft_cols_blk_kernel<double, 16, 512>));
+  NUS_ATTRW((fft_cols_blk_kernel<float, 16, 512>));
+  NUS_ATTRW((fft_cols_blk_kernel<double, 2, 512>));
+  NUS_ATTRW((fft_cols_blk_kernel<float, 2, 512>));
+  NUS_ATTRW((fft_rows_crop_kernel<double, double, 2, 512>));
+  NUS_ATTRW((fft_rows_crop_kernel<float, float, 2, 512>));
+  NUS_ATTRW((fft_rows_crop_kernel<float, double, 2, 512>));
+#undef NUS_ATTRW
+  const int smem2 = kBufs * kFftElems * static_cast<int>(sizeof(double2)) + kBufs * 8;
+#define NUS_ATTR2(KERN) NUS_CUDA(cudaFuncSetAttribute(KERN, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2))
+  NUS_ATTR2((fft_cols_async_kernel<double, 16>));
+  NUS_ATTR2((fft_cols_async_kernel<double, 8>));
+  NUS_ATTR2((fft_cols_async_kernel<double, 4>));
+  NUS_ATTR2((fft_cols_async_kernel<double, 2>));
+  NUS_ATTR2((fft_cols_async_kernel<float, 16>));
+  NUS_ATTR2((fft_cols_async_kernel<float, 8>));
+  NUS_ATTR2((fft_cols_async_kernel<float, 4>));
+  NUS_ATTR2((fft_cols_async_kernel<float, 2>));
+  NUS_ATTR2((fft_rows_crop_async_kernel<double, double, 16>));
+  NUS_ATTR2((fft_rows_crop_async_kernel<float, double, 16>));
+  NUS_ATTR2((fft_rows_crop_async_kernel<float, float, 16>));
+#undef NUS_ATTR2
+  if (dev < 64) done[dev] = true;
+}
+}  // namespace
 
 void fused_fft_prepare(Plan& plan) {
   PlanParams& p = plan.p;
   FusedFft& f = plan.ffft;
   if (!fused_fft_supported(p) || f.ready) return;
+  configure_fft_kernels();
   const int lg = ilog2(p.mr);
-  // 256 threads x 16 registers: every in-CTA FFT holds exactly 4096 elements.
-  // Rows: C = 4096 (pass B, one row per CTA); columns: R = Mr / 4096 with CW = 4096 / R
-  // consecutive columns per CTA (>= 128-byte row segments for R <= 512).
-  // 2048-point rows (pass B at 4 CTAs / SM) whenever the pass-A tile still holds whole
-  // columns (R = Mr / 2048 <= 4096); NUS_FFT_C=4096 keeps 4096-point rows
+  // Rows (pass B, one row per CTA): NT threads x 16 registers = C elements.  C = Mr for
+  // Mr <= 8192 (single pass, no pass A); 2048-point rows (4 CTAs / SM) for 2^14 <= Mr <= 2^23
+  // (NUS_FFT_C=4096 keeps 4096-point rows from 2^17); 4096 at 2^24; 8192 (512 threads) at 2^25, 2^26.
+  // Columns (pass A): R = Mr / C, one R x CW tile (contiguous in the blocked layout) per CTA.
   {
     const char* e = std::getenv("NUS_FFT_C");
     const bool c4096 = e && std::strcmp(e, "4096") == 0;
-    f.C = (!c4096 && p.mr >= (int64_t{1} << 17) && p.mr <= (int64_t{1} << 23)) ? kFftElems / 2 : kFftElems;
+    if (p.mr <= 2 * kFftElems) f.C = static_cast<int>(p.mr);
+    else if (p.mr <= (int64_t{1} << 23)) f.C = (c4096 && p.mr >= (int64_t{1} << 17)) ? kFftElems : kFftElems / 2;
+    else if (p.mr == (int64_t{1} << 24)) f.C = kFftElems;
+    else f.C = 2 * kFftElems;
   }
-  const bool wide = p.mr == (int64_t{1} << 25);  // 8192-element tiles and rows
-  if (wide) f.C = 2 * kFftElems;
+  const bool wide = f.C == 2 * kFftElems && p.mr > f.C;  // 8192-element tiles
   f.R = static_cast<int>(p.mr / f.C);
   f.RPC = 1;
   {  // pass A: register-loading 4096-cell tiles (default; 96.4 vs 107.4 us for the bulk-copy
@@ -756,19 +859,18 @@ void fused_fft_prepare(Plan& plan) {
     const char* e = std::getenv("NUS_FFT_COLS");
     f.cols_mode = (e && std::strcmp(e, "async") == 0) ? 2 : (e && std::strcmp(e, "reg128") == 0) ? 0 : 1;
   }
-  if (f.cols_mode == 0 && f.R > kFftElems / 2) f.cols_mode = 1;  // a 2048-cell tile must hold >= 1 column
-  if (wide) f.cols_mode = 3;  // R = 4096 rows x CW = 2 columns per 8192-cell tile
+  if (f.cols_mode == 0 && (f.R > kFftElems / 2 || f.R < 32)) f.cols_mode = 1;  // a 2048-cell tile must hold >= 1 column
+  if (f.cols_mode == 2 && f.R < 32) f.cols_mode = 1;
+  if (wide) f.cols_mode = 3;  // R = 4096 / 8192 rows x CW = 2 / 1 columns per 8192-cell tile
+  if (f.R > 1 && f.R <= 16) f.cols_mode = 4;  // short columns: register DFTs (fft_cols_small_kernel)
   const int tile = f.cols_mode == 0 ? kFftElems / 2 : f.cols_mode == 3 ? 2 * kFftElems : kFftElems;
   f.CW = f.R > 1 ? tile / f.R : 0;
   f.lo_bits = lg / 2;
-  // blocked grid layout + bulk-copy (asynchronous) passes unless NUS_FFT_ASYNC=0
-  {
-    const char* e = std::getenv("NUS_FFT_ASYNC");
-    f.blocked = f.R > 1 && !(e && std::strcmp(e, "0") == 0);
-    f.lgC = ilog2(f.C);
-    f.lgCW = f.CW > 0 ? ilog2(f.CW) : 0;
-    f.lgT = ilog2(f.R) + f.lgCW;
-  }
+  // blocked grid layout whenever there is a pass A (every pass-A tile contiguous)
+  f.blocked = f.R > 1;
+  f.lgC = ilog2(f.C);
+  f.lgCW = f.CW > 0 ? ilog2(f.CW) : 0;
+  f.lgT = ilog2(f.R) + f.lgCW;
   const bool f64 = p.precision == NUS_F64;
   const size_t cb = f64 ? sizeof(double2) : sizeof(float2);
   const int64_t hi_count = (p.mr >> f.lo_bits), lo_count = int64_t{1} << f.lo_bits;
@@ -792,51 +894,6 @@ void fused_fft_prepare(Plan& plan) {
   build(f.tw_c, f.C, 1, f.C);
   build(f.tw_hi, hi_count, lo_count, p.mr);
   build(f.tw_lo, lo_count, 1, p.mr);
-  static bool configured = false;
-  if (!configured) {
-    const int smem = kFftElems * static_cast<int>(sizeof(double2));
-#define NUS_ATTR(KERN) NUS_CUDA(cudaFuncSetAttribute(KERN, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))
-    NUS_ATTR((fft_cols_kernel<double, 16>));
-    NUS_ATTR((fft_cols_kernel<double, 8>));
-    NUS_ATTR((fft_cols_kernel<double, 4>));
-    NUS_ATTR((fft_cols_kernel<double, 2>));
-    NUS_ATTR((fft_rows_crop_kernel<double, double, 16>));
-    NUS_ATTR((fft_cols_blk_kernel<double, 16, kFftThreads>));
-    NUS_ATTR((fft_cols_blk_kernel<double, 8, kFftThreads>));
-    NUS_ATTR((fft_cols_blk_kernel<double, 4, kFftThreads>));
-    NUS_ATTR((fft_cols_blk_kernel<double, 2, kFftThreads>));
-    NUS_ATTR((fft_cols_blk_kernel<double, 4, kFftThreads, 6>));
-    NUS_ATTR((fft_cols_blk_kernel<double, 8, kFftThreads, 7>));
-    NUS_ATTR((fft_cols_blk_kernel<double, 16, kFftThreads, 8>));
-    NUS_ATTR((fft_cols_blk_kernel<double, 2, kFftThreads, 9>));
-    NUS_ATTR((fft_cols_blk_kernel<double, 4, kFftThreads, 10>));
-    NUS_ATTR((fft_cols_blk_kernel<double, 8, kFftThreads, 11>));
-    NUS_ATTR((fft_cols_blk_kernel<double, 16, kFftThreads, 12>));
-#undef NUS_ATTR
-    const int smem_w = 2 * kFftElems * static_cast<int>(sizeof(double2));
-#define NUS_ATTRW(KERN) NUS_CUDA(cudaFuncSetAttribute(KERN, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_w))
-    NUS_ATTRW((fft_cols_blk_kernel<double, 16, 512>));
-    NUS_ATTRW((fft_cols_blk_kernel<float, 16, 512>));
-    NUS_ATTRW((fft_rows_crop_kernel<double, double, 2, 512>));
-    NUS_ATTRW((fft_rows_crop_kernel<float, float, 2, 512>));
-    NUS_ATTRW((fft_rows_crop_kernel<float, double, 2, 512>));
-#undef NUS_ATTRW
-    const int smem2 = kBufs * kFftElems * static_cast<int>(sizeof(double2)) + kBufs * 8;
-#define NUS_ATTR2(KERN) NUS_CUDA(cudaFuncSetAttribute(KERN, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2))
-    NUS_ATTR2((fft_cols_async_kernel<double, 16>));
-    NUS_ATTR2((fft_cols_async_kernel<double, 8>));
-    NUS_ATTR2((fft_cols_async_kernel<double, 4>));
-    NUS_ATTR2((fft_cols_async_kernel<double, 2>));
-    NUS_ATTR2((fft_cols_async_kernel<float, 16>));
-    NUS_ATTR2((fft_cols_async_kernel<float, 8>));
-    NUS_ATTR2((fft_cols_async_kernel<float, 4>));
-    NUS_ATTR2((fft_cols_async_kernel<float, 2>));
-    NUS_ATTR2((fft_rows_crop_async_kernel<double, double, 16>));
-    NUS_ATTR2((fft_rows_crop_async_kernel<float, double, 16>));
-    NUS_ATTR2((fft_rows_crop_async_kernel<float, float, 16>));
-#undef NUS_ATTR2
-    configured = true;
-  }
   NUS_CUDA(cudaDeviceSynchronize());
   f.ready = true;
 }
@@ -851,7 +908,6 @@ int first_radix(int L) {
   return r == 0 ? 16 : (1 << r);
 }
 
-bool use_async(const FusedFft& f, size_t) { return f.blocked; }
 
 int sm_count() {
   static int sms = [] {
@@ -869,19 +925,36 @@ void launch_cols(const Plan& plan, void* grid, void* scratch, int64_t k, int64_t
   const FusedFft& f = plan.ffft;
   using T2 = typename C2<Real>::T;
   auto* g = static_cast<T2*>(grid);
+  auto* out = static_cast<T2*>(scratch);
   const T2 *tr = f.tw_r.as<T2>(), *th = f.tw_hi.as<T2>(), *tl = f.tw_lo.as<T2>();
   const int r0 = first_radix(f.R);
-  if (use_async(f, sizeof(T2)) && f.cols_mode != 2) {
-    const int64_t ntiles = p.channels * k * (f.C / f.CW);
-    auto* out = static_cast<T2*>(scratch);
+  const int64_t ntiles = p.channels * k * (f.C / f.CW);
+  if (f.cols_mode == 4) {  // R <= 16: register DFTs per column
+    const int lg_nblk = ilog2(f.C / f.CW);
+#define NUS_COLS_SMALL(RR)                                                                                     \
+  fft_cols_small_kernel<Real, RR><<<static_cast<unsigned>(ntiles), kFftThreads, 0, s>>>(                      \
+      static_cast<const T2*>(g), out, p.mr, f.C, f.CW, lg_nblk, static_cast<int>(k), static_cast<int>(kpad), th, \
+      tl, f.lo_bits, f.row_lo, f.row_cnt)
+    switch (f.R) {
+      case 2: NUS_COLS_SMALL(2); break;
+      case 4: NUS_COLS_SMALL(4); break;
+      case 8: NUS_COLS_SMALL(8); break;
+      case 16: NUS_COLS_SMALL(16); break;
+      default: fail(NUS_ERR_INVALID_ARGUMENT, "fft: unsupported short column length");
+    }
+#undef NUS_COLS_SMALL
+    return;
+  }
+  if (f.cols_mode != 2) {
 #define NUS_COLS_REG(R0, NT) NUS_COLS_REGL(R0, NT, 0)
 #define NUS_COLS_REGL(R0, NT, LG)                                                                            \
   launch_pdl(fft_cols_blk_kernel<Real, R0, NT, LG>, dim3(static_cast<unsigned>(ntiles)), dim3(NT),            \
              static_cast<size_t>(NT) * 16 * sizeof(T2), s, static_cast<const T2*>(g), out, p.mr, f.R, f.C, f.CW, \
              static_cast<int>(k), static_cast<int>(kpad), tr, th, tl, f.lo_bits, f.row_lo, f.row_cnt)
-    if (f.cols_mode == 3) {
-      require(r0 == 16, "fft: unexpected first radix for 8192-element tiles");
-      NUS_COLS_REG(16, 512);
+    if (f.cols_mode == 3) {  // R = 4096 (Mr = 2^25) or 8192 (2^26)
+      if (r0 == 16) NUS_COLS_REG(16, 512);
+      else if (r0 == 2) NUS_COLS_REG(2, 512);
+      else fail(NUS_ERR_INVALID_ARGUMENT, "fft: unexpected first radix for 8192-element tiles");
     } else if (f.cols_mode == 0) {
       if (r0 == 16) NUS_COLS_REG(16, 128);
       else if (r0 == 8) NUS_COLS_REG(8, 128);
@@ -907,33 +980,18 @@ void launch_cols(const Plan& plan, void* grid, void* scratch, int64_t k, int64_t
 #undef NUS_COLS_REGL
     return;
   }
-  if (use_async(f, sizeof(T2))) {
-    const int64_t ntiles = p.channels * k * (f.C / f.CW);
-    T2* out = static_cast<T2*>(scratch);
-    const unsigned grid_x = static_cast<unsigned>(std::min<int64_t>(ntiles, sm_count()));
-    const size_t smem = kBufs * static_cast<size_t>(kFftElems) * sizeof(T2) + kBufs * sizeof(uint64_t);
+  const unsigned grid_x = static_cast<unsigned>(std::min<int64_t>(ntiles, sm_count()));
+  const size_t smem = kBufs * static_cast<size_t>(kFftElems) * sizeof(T2) + kBufs * sizeof(uint64_t);
 #define NUS_COLS_ASYNC(R0)                                                                                   \
   fft_cols_async_kernel<Real, R0><<<grid_x, kFftThreads * kGroups, smem, s>>>(g, out, p.mr, f.R, f.C, f.CW, ntiles, \
                                                                     static_cast<int>(k), static_cast<int>(kpad), \
                                                                     tr, th, tl, f.lo_bits, f.row_lo, f.row_cnt, \
                                                                     f.zeros.as<T2>())
-    if (r0 == 16) NUS_COLS_ASYNC(16);
-    else if (r0 == 8) NUS_COLS_ASYNC(8);
-    else if (r0 == 4) NUS_COLS_ASYNC(4);
-    else NUS_COLS_ASYNC(2);
+  if (r0 == 16) NUS_COLS_ASYNC(16);
+  else if (r0 == 8) NUS_COLS_ASYNC(8);
+  else if (r0 == 4) NUS_COLS_ASYNC(4);
+  else NUS_COLS_ASYNC(2);
 #undef NUS_COLS_ASYNC
-    return;
-  }
-  const dim3 ga(static_cast<unsigned>(f.C / f.CW), static_cast<unsigned>(p.channels));
-  const size_t smem = static_cast<size_t>(f.R) * f.CW * sizeof(T2);
-#define NUS_COLS(R0)                                                                                   \
-  fft_cols_kernel<Real, R0><<<ga, kFftThreads, smem, s>>>(g, p.mr, f.R, f.C, f.CW, p.mr, static_cast<int>(k), \
-                                                          static_cast<int>(kpad), tr, th, tl, f.lo_bits)
-  if (r0 == 16) NUS_COLS(16);
-  else if (r0 == 8) NUS_COLS(8);
-  else if (r0 == 4) NUS_COLS(4);
-  else NUS_COLS(2);
-#undef NUS_COLS
 }
 
 template <typename Real, typename PReal>
@@ -949,7 +1007,7 @@ void launch_rows(const Plan& plan, void* grid, int64_t k, int64_t kpad, void* j_
   // The bulk-copy pass B is correct but measured slower than the register-loading kernel
   // on C2 (0.102 vs 0.097 ms): opt in with NUS_FFT_ASYNC_B=1.
   static const bool async_b = fused_pass_b_async();
-  if (use_async(f, sizeof(T2)) && r0 == 16 && f.C == kFftElems && async_b) {
+  if (f.blocked && r0 == 16 && f.C == kFftElems && async_b) {
     const int64_t nrows = p.channels * f.R;
     const unsigned grid_x = static_cast<unsigned>(std::min<int64_t>(nrows, sm_count()));
     const size_t smem_a = kBufs * static_cast<size_t>(kFftElems) * sizeof(T2) + kBufs * sizeof(uint64_t);
@@ -962,15 +1020,14 @@ void launch_rows(const Plan& plan, void* grid, int64_t k, int64_t kpad, void* j_
   launch_pdl(fft_rows_crop_kernel<Real, PReal, R0, NT>, gb, dim3(NT), smem, s, g, p.mr, f.R, f.C, 1, kpad, \
              static_cast<int>(k), p.nc, p.mode_offset, plan.tab.deconv.as<Real>(), f.tw_c.as<T2>(),       \
              static_cast<T2*>(j_out), static_cast<PReal*>(power), divisor, acc)
-  if (f.C == 2 * kFftElems) {  // 8192-point rows (Mr = 2^25), 512 threads
-    require(r0 == 2, "fft: unexpected first radix for 8192-point rows");
-    NUS_ROWS(2, 512);
-  } else if (f.C == kFftElems / 2) {  // 2048-point rows, 128 threads
-    NUS_ROWS(8, 128);
-  } else if (r0 == 16) NUS_ROWS(16, kFftThreads);
-  else if (r0 == 8) NUS_ROWS(8, kFftThreads);
-  else if (r0 == 4) NUS_ROWS(4, kFftThreads);
-  else NUS_ROWS(2, kFftThreads);
+  switch (f.C) {  // C = NT * 16; the first radix makes the remaining stages radix 16
+    case 512: NUS_ROWS(2, 32); break;
+    case 1024: NUS_ROWS(4, 64); break;
+    case 2048: NUS_ROWS(8, 128); break;
+    case 4096: NUS_ROWS(16, kFftThreads); break;
+    case 8192: NUS_ROWS(2, 512); break;
+    default: fail(NUS_ERR_INVALID_ARGUMENT, "fft: unsupported row length");
+  }
 #undef NUS_ROWS
 }
 
@@ -983,21 +1040,63 @@ bool fused_pass_b_async() {
 
 void fft_stage_names(const Plan& plan, const char** a, const char** b) {
   if (!plan.ffft.ready) {
-    *a = "cufft (library)";
+    *a = "stockham_r2_kernel";
     *b = "crop_power_kernel";
     return;
   }
-  *a = plan.ffft.R <= 1          ? "(none: single pass)"
-       : !plan.ffft.blocked        ? "fft_cols_kernel"
+  *a = plan.ffft.R <= 1            ? "(none: single pass)"
+       : plan.ffft.cols_mode == 4  ? "fft_cols_small_kernel"
        : plan.ffft.cols_mode == 2  ? "fft_cols_async_kernel"
                                    : "fft_cols_blk_kernel";
   *b = (plan.ffft.blocked && fused_pass_b_async()) ? "fft_rows_crop_async_kernel" : "fft_rows_crop_kernel";
 }
 
+void fft_generic_rows(void* data, int64_t n, int64_t rows, int64_t k, int64_t kpad, bool f64, bool inverse,
+                      void* scratch, cudaStream_t s) {
+  require(n >= 1 && (n & (n - 1)) == 0, "fft: size must be a power of two");
+  if (n == 1 || rows == 0) return;
+  const int stages = ilog2(n);
+  const int64_t work = rows * (n / 2);
+  const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((work + 255) / 256, int64_t{148} * 16));
+  void* bufs[2] = {data, scratch};
+  const int64_t kp[2] = {kpad, k};  // data: [C][kpad][n] (first k rows per channel); scratch dense
+  for (int st = 0; st < stages; ++st) {
+    const int in = st & 1, out = in ^ 1;
+    const int64_t ns = int64_t{1} << st;
+    if (f64)
+      stockham_r2_kernel<double2><<<blocks, 256, 0, s>>>(static_cast<const double2*>(bufs[in]),
+                                                         static_cast<double2*>(bufs[out]), n, ns, rows, k, kp[in],
+                                                         kp[out], inverse ? 1 : 0);
+    else
+      stockham_r2_kernel<float2><<<blocks, 256, 0, s>>>(static_cast<const float2*>(bufs[in]),
+                                                        static_cast<float2*>(bufs[out]), n, ns, rows, k, kp[in],
+                                                        kp[out], inverse ? 1 : 0);
+    note_launch();
+    check_launch("stockham_r2_kernel");
+  }
+  if (stages & 1) {  // the result is in the scratch: back to the caller's layout
+    const unsigned cb = static_cast<unsigned>(std::min<int64_t>((rows * n + 255) / 256, int64_t{148} * 16));
+    if (f64)
+      copy_rows_kernel<double2><<<cb, 256, 0, s>>>(static_cast<const double2*>(scratch), static_cast<double2*>(data),
+                                                   n, rows, k, k, kpad);
+    else
+      copy_rows_kernel<float2><<<cb, 256, 0, s>>>(static_cast<const float2*>(scratch), static_cast<float2*>(data), n,
+                                                  rows, k, k, kpad);
+    note_launch();
+    check_launch("copy_rows_kernel");
+  }
+}
+
+void fft_generic_inplace(void* data, int64_t n, int64_t batch, bool f64, bool inverse, cudaStream_t s) {
+  DeviceBuffer scratch(static_cast<size_t>(n) * batch * (f64 ? sizeof(double2) : sizeof(float2)));
+  fft_generic_rows(data, n, batch, batch, batch, f64, inverse, scratch.ptr, s);
+  NUS_CUDA(cudaStreamSynchronize(s));  // scratch is released at scope end
+}
+
 void run_fused_pass_a(Plan& plan, void* grid, int64_t k, int64_t kpad, cudaStream_t s) {
   if (plan.ffft.R <= 1) return;
   void* scratch = nullptr;
-  if (plan.ffft.blocked) {  // pass A writes the natural layout out of place; pass B reads it there
+  {  // pass A writes the natural layout out of place; pass B reads it there
     const size_t need = static_cast<size_t>(plan.p.channels * kpad * plan.p.mr) *
                         (plan.p.precision == NUS_F64 ? sizeof(double2) : sizeof(float2));
     if (plan.ffft.scratch.bytes < need) {
@@ -1009,12 +1108,12 @@ void run_fused_pass_a(Plan& plan, void* grid, int64_t k, int64_t kpad, cudaStrea
   if (plan.p.precision == NUS_F64) launch_cols<double>(plan, grid, scratch, k, kpad, s);
   else launch_cols<float>(plan, grid, scratch, k, kpad, s);
   note_launch();
-  check_launch("fft_cols_kernel");
+  check_launch("fft pass A");
 }
 
 void run_fused_pass_b(Plan& plan, void* grid, int64_t k, int64_t kpad, void* j_out, void* power, bool power_f64,
                       double divisor, bool accumulate, cudaStream_t s) {
-  if (plan.ffft.blocked && plan.ffft.R > 1) grid = plan.ffft.scratch.ptr;  // pass A's output
+  if (plan.ffft.R > 1) grid = plan.ffft.scratch.ptr;  // pass A's output
   const int acc = accumulate ? 1 : 0;
   if (plan.p.precision == NUS_F64) launch_rows<double, double>(plan, grid, k, kpad, j_out, power, divisor, acc, s);
   else if (power_f64) launch_rows<float, double>(plan, grid, k, kpad, j_out, power, divisor, acc, s);

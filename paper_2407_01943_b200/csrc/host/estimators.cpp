@@ -43,6 +43,7 @@ SpectrumEstimate::SpectrumEstimate(BandPlan p, std::vector<double> pw, Estimator
 struct MtnufftEstimator::Built {
   std::shared_ptr<nus_mtnufft_s> handle;
   TaperSet tapers;
+  std::shared_ptr<nus_mtnufft_multi_s> multi;
 };
 
 namespace {
@@ -85,9 +86,24 @@ MtnufftEstimator::Built MtnufftEstimator::build(const SamplingGrid& grid, const 
     std::vector<double> w(k * n);
     for (std::size_t j = 0; j < k; ++j) std::copy(ts.weights_real(j).begin(), ts.weights_real(j).end(), w.begin() + j * n);
     host::check(nus_mtnufft_create(&cfg, grid.times().data(), centers.data(), w.data(), &h));
-    return {wrap(h), std::move(ts)};
+    return {wrap(h), std::move(ts), nullptr};
   }
   if (k < 1 || k > n) throw std::invalid_argument("dpss_uniform: k_tapers out of range");
+  if (o.devices.size() > 1) {  // one series over several GPUs (multi.cu)
+    nus_mtnufft_multi_t mh = nullptr;
+    const std::vector<int32_t> devs(o.devices.begin(), o.devices.end());
+    host::check(nus_mtnufft_multi_create(&cfg, devs.data(), static_cast<int32_t>(devs.size()),
+                                         o.sharding == Sharding::tapers ? NUS_SHARD_TAPERS : NUS_SHARD_SAMPLES,
+                                         grid.times().data(), centers.data(), nullptr, nullptr, &mh));
+    std::shared_ptr<nus_mtnufft_multi_s> multi(mh, [](nus_mtnufft_multi_s* p) { nus_mtnufft_multi_destroy(p); });
+    std::vector<double> w(k * n);
+    host::check(nus_mtnufft_multi_tapers(multi.get(), w.data()));
+    std::vector<std::vector<std::complex<double>>> weights(k, std::vector<std::complex<double>>(n));
+    for (std::size_t j = 0; j < k; ++j)
+      for (std::size_t i = 0; i < n; ++i) weights[j][i] = {w[j * n + i], 0.0};
+    return {nullptr, TaperSet(grid, AnalysisBand(0.0, plan.half_width()), band.f_max, std::move(weights), {}, true),
+            std::move(multi)};
+  }
   host::check(nus_mtnufft_create(&cfg, grid.times().data(), centers.data(), nullptr, &h));
   auto handle = wrap(h);
   std::vector<double> w(k * n);
@@ -96,7 +112,7 @@ MtnufftEstimator::Built MtnufftEstimator::build(const SamplingGrid& grid, const 
   for (std::size_t j = 0; j < k; ++j)
     for (std::size_t i = 0; i < n; ++i) weights[j][i] = {w[j * n + i], 0.0};
   return {std::move(handle),
-          TaperSet(grid, AnalysisBand(0.0, plan.half_width()), band.f_max, std::move(weights), {}, true)};
+          TaperSet(grid, AnalysisBand(0.0, plan.half_width()), band.f_max, std::move(weights), {}, true), nullptr};
 }
 
 MtnufftEstimator::MtnufftEstimator(const SamplingGrid& grid, const SignalBand& signal_band, const BandPlan& plan,
@@ -105,13 +121,19 @@ MtnufftEstimator::MtnufftEstimator(const SamplingGrid& grid, const SignalBand& s
 
 MtnufftEstimator::MtnufftEstimator(const SamplingGrid& grid, const BandPlan& plan, const Options& opts,
                                    Built&& built)
-    : grid_(grid), plan_(plan), opts_(opts), handle_(std::move(built.handle)), tapers_(std::move(built.tapers)) {}
+    : grid_(grid),
+      plan_(plan),
+      opts_(opts),
+      handle_(std::move(built.handle)),
+      multi_(std::move(built.multi)),
+      tapers_(std::move(built.tapers)) {}
 
 SpectrumEstimate MtnufftEstimator::estimate(const std::vector<double>& values) const {
   if (values.size() != grid_.n_samples())
     throw std::invalid_argument("estimate: series length does not match grid");
   std::vector<double> power(plan_.size());
-  host::check(nus_mtnufft_estimate(handle_.get(), values.data(), power.data()));
+  if (multi_) host::check(nus_mtnufft_multi_estimate(multi_.get(), values.data(), power.data()));
+  else host::check(nus_mtnufft_estimate(handle_.get(), values.data(), power.data()));
   const std::size_t bands = plan_.size();
   return SpectrumEstimate(plan_, std::move(power), method(),
                           std::vector<std::size_t>(bands, opts_.k_tapers),

@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "nus_estimator.cuh"
@@ -72,7 +73,8 @@ void validate_grid(const double* times, int64_t channels, int64_t n) {
 }  // namespace
 
 std::unique_ptr<Estimator> estimator_create(const nus_mtnufft_config_t& cfg, const double* times,
-                                            const double* centers, const double* tapers) {
+                                            const double* centers, const double* tapers,
+                                            const double* f_w_channels) {
   require(cfg.channels >= 1, "MtnufftEstimator: channels must be >= 1");
   require(cfg.k_tapers >= 1, "MtnufftEstimator: k_tapers must be >= 1");
   require(times && centers, "MtnufftEstimator: null input");
@@ -80,6 +82,11 @@ std::unique_ptr<Estimator> estimator_create(const nus_mtnufft_config_t& cfg, con
   use_device(cfg.device);
   auto est = std::make_unique<Estimator>();
   est->cfg = cfg;
+  est->f_w.assign(static_cast<size_t>(cfg.channels), cfg.f_w);
+  if (f_w_channels) {
+    for (int64_t c = 0; c < cfg.channels; ++c) est->f_w[c] = f_w_channels[c];
+    est->cfg.f_w = f_w_channels[0];
+  }
   const auto t_all = std::chrono::steady_clock::now();
   const int64_t C = cfg.channels, n = cfg.n, K = cfg.k_tapers;
   cudaStream_t s = 0;
@@ -94,7 +101,7 @@ std::unique_ptr<Estimator> estimator_create(const nus_mtnufft_config_t& cfg, con
     for (int64_t c = 0; c < C; ++c) {
       NUS_CUDA(cudaMemcpy(dt.ptr, times + c * n, n * sizeof(double), cudaMemcpyHostToDevice));
       double a = 0, b = 0, d = 0;
-      gpss_interpolated_device(dt.as<double>(), times + c * n, n, cfg.f_max, cfg.f_w, K,
+      gpss_interpolated_device(dt.as<double>(), times + c * n, n, cfg.f_max, est->f_w[c], K,
                                est->tapers_time.as<double>() + c * K * n, s, &a, &b, &d);
       est->setup_ms[0] += a;
       est->setup_ms[1] += b;

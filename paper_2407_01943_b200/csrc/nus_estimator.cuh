@@ -7,6 +7,7 @@ namespace nus {
 
 struct Estimator {
   nus_mtnufft_config_t cfg{};
+  std::vector<double> f_w;     // per-channel taper half-bandwidth (cfg.f_w unless given per channel)
   std::unique_ptr<Plan> plan;
   DeviceBuffer tapers_time;    // fp64 [C][K][n], time order (normalised)
   DeviceBuffer tapers_sorted;  // plan precision [C][K][n], start-cell order
@@ -28,8 +29,10 @@ struct Estimator {
   ~Estimator();
 };
 
+// f_w_channels: [channels] per-channel half-bandwidths, or null for cfg.f_w on every channel
 std::unique_ptr<Estimator> estimator_create(const nus_mtnufft_config_t& cfg, const double* times,
-                                            const double* centers, const double* tapers);
+                                            const double* centers, const double* tapers,
+                                            const double* f_w_channels = nullptr);
 void estimator_run(Estimator& est, const void* x_dev, int x_dtype, void* power_dev, bool power_f64,
                    void* j_dev, cudaStream_t s);
 void estimator_estimate_batch_host(Estimator& est, const double* x, int64_t steps, double* power);
@@ -38,6 +41,19 @@ void estimator_timing_enable(Estimator& est, size_t max_runs);
 void estimator_timing_read(Estimator& est, double* ms3, int64_t* runs);
 void estimator_bytes(const Estimator& est, int x_dtype, double* total, double* spread, double* fft,
                      double* crop);
+
+// Multi-GPU estimator in one process (multi.cu)
+struct MultiEstimator;
+struct MultiDeleter {
+  void operator()(MultiEstimator* m) const;
+};
+using MultiPtr = std::unique_ptr<MultiEstimator, MultiDeleter>;
+MultiPtr multi_create(const nus_mtnufft_config_t& cfg, const int32_t* devices, int32_t n_devices,
+                                             int32_t sharding, const double* times, const double* centers,
+                                             const double* f_w, const double* tapers);
+void multi_estimate(MultiEstimator& m, const double* x_host, double* power_host);
+int64_t multi_peer_bytes(const MultiEstimator& m);
+void multi_tapers(const MultiEstimator& m, double* out_host);
 
 double f_quantile_host(double p, int64_t d1, int64_t d2);
 void ftest_device(const void* j_dev, bool j_f32, int64_t k, int64_t nb, int64_t channels, const double* w0_host,

@@ -3,7 +3,6 @@
 
 #include <cuda_runtime.h>
 #include <utility>
-#include <cufft.h>
 
 #include <atomic>
 #include <cstdint>
@@ -33,9 +32,7 @@ inline void require(bool ok, const std::string& msg) {
 }
 
 void cuda_check(cudaError_t e, const char* what);
-void cufft_check(cufftResult r, const char* what);
 #define NUS_CUDA(x) ::nus::cuda_check((x), #x)
-#define NUS_CUFFT(x) ::nus::cufft_check((x), #x)
 
 // Count of our own kernel launches (the bench reports it as gpu_launches).
 extern std::atomic<int64_t> g_launches;
@@ -133,15 +130,6 @@ struct SpreadTables {
   DeviceBuffer first_cell;      // int64 [C][n] reference j0, time order (kept for parity queries)
 };
 
-class FftCache {
- public:
-  cufftHandle get(int64_t mr, int64_t batch, int precision);
-  ~FftCache();
- private:
-  struct Entry { int64_t mr, batch; int precision; cufftHandle h; };
-  std::vector<Entry> entries_;
-};
-
 // Tables of the fused two-pass FFT (fft.cu): Mr = R * C, twiddles e^{-2 pi i m / L}.
 struct FusedFft {
   bool ready = false;
@@ -171,8 +159,7 @@ struct Plan {
   DeviceBuffer d_times;         // fp64 [C][n]
   DeviceBuffer d_centers;       // fp64 [I]
   SpreadTables tab;
-  FftCache fft;
-  std::mutex mu;                // serialises use of the default workspace + cuFFT plans
+  std::mutex mu;                // serialises use of the default workspace
   DeviceBuffer work;            // default grid workspace
 };
 
@@ -214,8 +201,15 @@ void run_fft(Plan& plan, void* grid, int64_t k, int64_t kpad, cudaStream_t s);
 void run_crop(Plan& plan, void* grid, int64_t k, int64_t kpad, void* j_out, void* power,
               bool power_f64, double divisor, bool accumulate, cudaStream_t s);
 
-// Fused two-pass FFT + crop/power (fft.cu); supported for 32 <= Mr <= 2^24.
+// Fused two-pass FFT + crop/power (fft.cu); 512 <= Mr <= 2^26 (else the generic radix-2 kernels).
 bool fused_fft_supported(const PlanParams& p);
+// Generic radix-2 Stockham FFT (fft.cu), one launch per stage: `rows` rows of length n (power of
+// two), row r at ((r / k) kpad + r % k) n, transformed in place (forward e^{-2 pi i jk/n}, inverse
+// the conjugate transform without 1/n, as Radix2Fft); scratch holds rows * n complex elements.
+void fft_generic_rows(void* data, int64_t n, int64_t rows, int64_t k, int64_t kpad, bool f64, bool inverse,
+                      void* scratch, cudaStream_t s);
+// Same for `batch` contiguous rows, allocating its own scratch (synchronises s).
+void fft_generic_inplace(void* data, int64_t n, int64_t batch, bool f64, bool inverse, cudaStream_t s);
 // MTNUFFT0 (gep.cu)
 void generalized_eigen_device(const double* d_are, const double* d_aim, const double* d_m, int64_t n, int64_t k,
                               double ridge_first, double ridge_retry, bool want_vectors, double* values,

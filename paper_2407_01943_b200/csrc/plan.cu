@@ -27,12 +27,6 @@ void cuda_check(cudaError_t e, const char* what) {
   fail(NUS_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-void cufft_check(cufftResult r, const char* what) {
-  if (r == CUFFT_SUCCESS) return;
-  if (r == CUFFT_ALLOC_FAILED) fail(NUS_ERR_OUT_OF_MEMORY, std::string("cuFFT allocation: ") + what);
-  fail(NUS_ERR_CUDA, std::string("cuFFT error ") + std::to_string(static_cast<int>(r)) + ": " + what);
-}
-
 void check_launch(const char* what) { cuda_check(cudaGetLastError(), what); }
 
 void use_device(int device) {
@@ -61,23 +55,6 @@ void DeviceBuffer::release() {
   if (ptr) cudaFree(ptr);
   ptr = nullptr;
   bytes = 0;
-}
-
-FftCache::~FftCache() {
-  for (auto& e : entries_) cufftDestroy(e.h);
-}
-
-cufftHandle FftCache::get(int64_t mr, int64_t batch, int precision) {
-  for (auto& e : entries_)
-    if (e.mr == mr && e.batch == batch && e.precision == precision) return e.h;
-  cufftHandle h;
-  NUS_CUFFT(cufftCreate(&h));
-  long long n[1] = {mr};
-  size_t ws = 0;
-  const cufftType type = precision == NUS_F64 ? CUFFT_Z2Z : CUFFT_C2C;
-  NUS_CUFFT(cufftMakePlanMany64(h, 1, n, nullptr, 1, mr, nullptr, 1, mr, type, batch, &ws));
-  entries_.push_back({mr, batch, precision, h});
-  return h;
 }
 
 // ---- parameter selection (host; must reproduce the reference exactly) -------
@@ -400,8 +377,9 @@ void plan_build_tables(Plan& plan, cudaStream_t st) {
   note_launch();
   check_launch("deconv_kernel");
   NUS_CUDA(cudaStreamSynchronize(st));
+  // NUS_FFT=generic forces the generic radix-2 kernels (test hook for every grid size)
   const char* fft_env = std::getenv("NUS_FFT");
-  if (!(fft_env && std::strcmp(fft_env, "cufft") == 0)) fused_fft_prepare(plan);
+  if (!(fft_env && std::strcmp(fft_env, "generic") == 0)) fused_fft_prepare(plan);
   FusedFft& ff = plan.ffft;
   ff.row_lo = 0;
   ff.row_cnt = ff.R;

@@ -551,12 +551,13 @@ __global__ void __launch_bounds__(kTcWarps * 32, G == 1 ? (sizeof(Real) == 8 ? 4
       for (int gg = 0; gg < G; ++gg) {
         R2* out0 = out + off_h0 + static_cast<int64_t>(8 * gg) * P.mr;
         R2* out1 = out + off_h1 + static_cast<int64_t>(8 * gg) * P.mr;
-        if (P.slots) {  // taper k -> owner k / per, its slot row k % per (possibly a peer GPU)
-          const int64_t ka = P.k0 + 8 * gg + 2 * t, kb = ka + 1;
+        const bool k0ok = 8 * gg + 2 * t < P.kg, k1ok = 8 * gg + 2 * t + 1 < P.kg;
+        if (P.slots) {  // taper k -> owner k / per, its slot row k % per (possibly a peer GPU);
+                        // padding lanes (k >= kg, never stored) read the table at k0 only
+          const int64_t ka = P.k0 + (k0ok ? 8 * gg + 2 * t : 0), kb = P.k0 + (k1ok ? 8 * gg + 2 * t + 1 : 0);
           out0 = P.slots[ka / P.per] + (ka % P.per) * P.mr;
           out1 = P.slots[kb / P.per] + (kb % P.per) * P.mr;
         }
-        const bool k0ok = 8 * gg + 2 * t < P.kg, k1ok = 8 * gg + 2 * t + 1 < P.kg;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
           const int addr = cell_addr32(cell0 + 8 * b, P.blocked, P.lgC, P.lgCW, P.lgT);

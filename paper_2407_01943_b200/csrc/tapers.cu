@@ -1204,23 +1204,16 @@ void dpss_concentrations(int64_t n, double tw, int64_t k, const double* d_vec, d
   sinc_symbol_kernel<<<blocks_for(L, 256), 256, 0, s>>>(n, L, wband, a.as<double2>());
   embed_kernel<<<blocks_for(L * k, 256), 256, 0, s>>>(d_vec, n, L, static_cast<int>(k), b.as<double2>());
   note_launch(2);
-  cufftHandle h1, hk;
-  NUS_CUFFT(cufftPlan1d(&h1, static_cast<int>(L), CUFFT_Z2Z, 1));
-  NUS_CUFFT(cufftPlan1d(&hk, static_cast<int>(L), CUFFT_Z2Z, static_cast<int>(k)));
-  NUS_CUFFT(cufftSetStream(h1, s));
-  NUS_CUFFT(cufftSetStream(hk, s));
-  NUS_CUFFT(cufftExecZ2Z(h1, a.as<cufftDoubleComplex>(), a.as<cufftDoubleComplex>(), CUFFT_FORWARD));
-  NUS_CUFFT(cufftExecZ2Z(hk, b.as<cufftDoubleComplex>(), b.as<cufftDoubleComplex>(), CUFFT_FORWARD));
+  fft_generic_inplace(a.ptr, L, 1, true, false, s);
+  fft_generic_inplace(b.ptr, L, k, true, false, s);
   cmul_kernel<<<blocks_for(L * k, 256), 256, 0, s>>>(b.as<double2>(), a.as<double2>(), L, static_cast<int>(k));
   note_launch();
-  NUS_CUFFT(cufftExecZ2Z(hk, b.as<cufftDoubleComplex>(), b.as<cufftDoubleComplex>(), CUFFT_INVERSE));
+  fft_generic_inplace(b.ptr, L, k, true, true, s);
   conc_dot_kernel<<<static_cast<unsigned>(k), 256, 0, s>>>(d_vec, b.as<double2>(), n, L, out.as<double>());
   note_launch();
   check_launch("dpss_concentrations");
   NUS_CUDA(cudaMemcpyAsync(conc, out.ptr, k * sizeof(double), cudaMemcpyDeviceToHost, s));
   NUS_CUDA(cudaStreamSynchronize(s));
-  cufftDestroy(h1);
-  cufftDestroy(hk);
   for (int64_t j = 0; j < k; ++j) conc[j] = std::min(std::max(conc[j], 0.0), 1.0);  // tapers.cpp:76
 }
 

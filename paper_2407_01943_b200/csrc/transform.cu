@@ -1,6 +1,9 @@
-// Library path (Mr > 2^24 or NUS_FFT=cufft): uniform FFT of the K oversampled grids (cuFFT, batched Z2Z / C2C forward,
-// e^{-2 pi i jk/Mr} as Radix2Fft::forward, src/fft.cpp:39-58) followed by one
-// fused deconvolve / crop / eigenspectrum kernel:
+// The FFT + crop entry points of the path (run_fft / run_crop / run_transform).
+//
+// Fused path (fft.cu, 512 <= Mr <= 2^26): pass A here, pass B fused with the crop and the
+// eigenspectrum reduction.  Other grid sizes: the generic radix-2 Stockham kernels
+// (e^{-2 pi i jk/Mr} as Radix2Fft::forward, src/fft.cpp:39-58) followed by one fused
+// deconvolve / crop / eigenspectrum kernel:
 //     J_k(i) = deconv_i * B_k[(-m_i) mod Mr],  m_i = i - I/2   (src/nufft.cpp:131-140,161-164)
 //     P(i)   = (sum_k |J_k(i)|^2) / K                           (src/estimators.cpp:113-117)
 // The power reduction over tapers happens in registers, so J never has to be
@@ -45,35 +48,18 @@ __global__ void crop_power_kernel(const typename V2<Real>::T* __restrict__ grid,
 }  // namespace
 
 void run_fft(Plan& plan, void* grid, int64_t k, int64_t kpad, cudaStream_t s) {
-  if (plan.ffft.ready) {  // custom two-pass FFT: pass A here, pass B fused with the crop
+  if (plan.ffft.ready) {  // fused two-pass FFT: pass A here, pass B fused with the crop
     run_fused_pass_a(plan, grid, k, kpad, s);
     return;
   }
   const PlanParams& p = plan.p;
   const bool f64 = p.precision == NUS_F64;
-  const size_t cbytes = f64 ? sizeof(double2) : sizeof(float2);
-  if (k == kpad || p.channels == 1) {
-    cufftHandle h = plan.fft.get(p.mr, k == kpad ? p.channels * k : k, p.precision);
-    NUS_CUFFT(cufftSetStream(h, s));
-    if (f64)
-      NUS_CUFFT(cufftExecZ2Z(h, static_cast<cufftDoubleComplex*>(grid),
-                             static_cast<cufftDoubleComplex*>(grid), CUFFT_FORWARD));
-    else
-      NUS_CUFFT(cufftExecC2C(h, static_cast<cufftComplex*>(grid), static_cast<cufftComplex*>(grid),
-                             CUFFT_FORWARD));
-  } else {
-    cufftHandle h = plan.fft.get(p.mr, k, p.precision);
-    NUS_CUFFT(cufftSetStream(h, s));
-    for (int64_t c = 0; c < p.channels; ++c) {
-      char* base = static_cast<char*>(grid) + c * kpad * p.mr * cbytes;
-      if (f64)
-        NUS_CUFFT(cufftExecZ2Z(h, reinterpret_cast<cufftDoubleComplex*>(base),
-                               reinterpret_cast<cufftDoubleComplex*>(base), CUFFT_FORWARD));
-      else
-        NUS_CUFFT(cufftExecC2C(h, reinterpret_cast<cufftComplex*>(base),
-                               reinterpret_cast<cufftComplex*>(base), CUFFT_FORWARD));
-    }
+  const size_t need = static_cast<size_t>(p.channels * k * p.mr) * (f64 ? sizeof(double2) : sizeof(float2));
+  if (plan.ffft.scratch.bytes < need) {
+    NUS_CUDA(cudaStreamSynchronize(s));
+    plan.ffft.scratch.alloc(need);
   }
+  fft_generic_rows(grid, p.mr, p.channels * k, k, kpad, f64, false, plan.ffft.scratch.ptr, s);
 }
 
 void run_crop(Plan& plan, void* grid, int64_t k, int64_t kpad, void* j_out, void* power,

@@ -103,6 +103,14 @@ class DeviceEngine:
                                                  row1, self.device, C.dptr(q)))
         return q
 
+    def quadform_fast(self, times, f_max, w):
+        """All K forms w^T R(B) w in O(N log N) (normalise.cu), the single-GPU setup's method."""
+        t, w = C.f64(times), C.f64(w)
+        q = np.empty(w.shape[0])
+        C.check(C.lib().nus_signal_band_quadform_fast(C.dptr(t), t.size, f_max, C.dptr(w), w.shape[0],
+                                                      self.device, C.dptr(q)))
+        return q
+
     # estimator ---------------------------------------------------------------
     def create(self, times, centers, f_max, f_w, k, eps, precision, tapers):
         from .api import _Estimator
@@ -143,18 +151,12 @@ class DeviceEngine:
 
     def ipc_handle(self, t):
         """(64-byte CUDA IPC handle of the allocation holding t, byte offset of t in it).  The
-        caching allocator may place t inside a larger cudaMalloc segment; torch's own sharing
-        call reports that offset (cudaIpcOpenMemHandle maps the segment base)."""
-        try:
-            info = t.untyped_storage()._share_cuda_()
-            handle, offset = bytes(info[1]), int(info[3]) + t.storage_offset() * t.element_size()
-            if len(handle) == 64:
-                return handle, offset
-        except Exception:  # pragma: no cover - older torch
-            pass
+        caching allocator may place t inside a larger cudaMalloc segment and cudaIpcOpenMemHandle
+        maps the segment base, so the offset is part of the handle (cuMemGetAddressRange)."""
         buf = ctypes.create_string_buffer(64)
-        C.check(C.lib().nus_ipc_get_handle(t.data_ptr(), buf))
-        return buf.raw, 0
+        off = ctypes.c_int64()
+        C.check(C.lib().nus_ipc_get_handle_offset(t.data_ptr(), buf, ctypes.byref(off)))
+        return buf.raw, int(off.value)
 
     def ipc_open(self, handle) -> int:
         raw, offset = handle
@@ -201,9 +203,10 @@ class ChannelShard:
         f_w = np.broadcast_to(np.asarray(f_w, dtype=np.float64), (self.channels,))
         self.est = None
         if self.c1 > self.c0:
-            # one batch estimator per rank: channels share n, centres, K, eps (tapers are per channel)
-            self.est = self.engine.create(times[self.c0:self.c1], centers, f_max, float(f_w[self.c0]), k, eps,
-                                          precision, None)
+            # one batch estimator per rank: channels share n, centres, K, eps; each channel's tapers
+            # are built on its own grid with its OWN half-bandwidth (P must not depend on the rank)
+            self.est = self.engine.create(times[self.c0:self.c1], centers, f_max,
+                                          np.ascontiguousarray(f_w[self.c0:self.c1]), k, eps, precision, None)
         self.nc = len(centers)
 
     def estimate_local(self, x_local, power_local):
@@ -262,6 +265,8 @@ class TaperShard:
 class SampleSplit:
     """Config C4: one long series, samples split across ranks, reduce-scatter of fine grids."""
 
+    fast_normalise_min = 1 << 18  # above this N the R(B) forms use the O(N log N) method
+
     def __init__(self, times, centers, f_max, f_w, k, eps, precision="f64", engine=None, group=None,
                  tapers: Optional[np.ndarray] = None, fused: Optional[bool] = None):
         import torch.distributed as dist
@@ -298,12 +303,17 @@ class SampleSplit:
             self.grid = self.engine.zeros((self.kpad, self.mr * 2), self.real)
 
     def _setup_slots(self):
-        """Receive slots [G][per][Mr] on every rank; this rank's slot pointer in every owner's
-        buffer (CUDA IPC peer mappings, exchanged with all_gather_object)."""
+        """Receive slots [2][G][per][Mr] on every rank (two parities, alternated per spectrum);
+        this rank's slot pointer in every owner's buffer for each parity (CUDA IPC peer mappings,
+        exchanged with all_gather_object).
+
+        Double buffering closes the write-after-read window: spectrum i+1 stores into the other
+        parity, and spectrum i+2 (same parity as i) starts only after the flag all_reduce of
+        spectrum i+1, which every owner reaches after its sum_slots of spectrum i (stream order)."""
         import torch
         g, r, per, mr = self.world, self.rank, self.per_rank, self.mr
         alloc = getattr(self.engine, "alloc_slots", self.engine.zeros)
-        self.recv = alloc((g, per, mr * 2), self.real)
+        self.recv = alloc((2, g, per, mr * 2), self.real)
         csize = 2 * self.recv.element_size()
         if g > 1:
             handles = [None] * g
@@ -313,8 +323,9 @@ class SampleSplit:
         else:
             self.peers = {}
             bases = [self.recv.data_ptr()]
-        ptrs = [b + r * per * mr * csize for b in bases]
+        ptrs = [[b + (par * g + r) * per * mr * csize for b in bases] for par in range(2)]
         self.slot_ptrs = torch.tensor(ptrs, dtype=torch.int64, device=self.recv.device)
+        self.parity = 0
         self.flag = torch.zeros(1, dtype=self.real, device=self.recv.device)
 
     def close(self):
@@ -343,18 +354,30 @@ class SampleSplit:
         self.engine.set_grid_rows(self.est, new_lo, new_cnt)
 
     def _normalised_tapers(self, times, f_max, f_w, k):
-        """Interpolated DPSS on the full grid + row-split R(B) normalisation (all_reduce of K sums)."""
+        """Interpolated DPSS on the full grid + the R(B) normalisation w^T R(B) w = 2 f_w.
+
+        N > 2^18 (C4): the O(N log N) form (normalise.cu, as the single-GPU setup) on rank 0,
+        broadcast so every rank holds bit-identical tapers.  Smaller N: the dense form, row-split
+        over the ranks (balanced triangle rows) + an all_reduce of the K partial sums."""
         import torch
         w = self.engine.taper_spline(times, f_max, f_w, k)
-        rows = balanced_triangle_rows(times.size, self.world)
-        q = np.zeros(k)
-        for k0 in range(0, k, 8):
-            q[k0:k0 + 8] = self.engine.quadform_rows(times, f_max, w[k0:k0 + 8], rows[self.rank],
-                                                     rows[self.rank + 1])
-        qt = torch.tensor(q, dtype=torch.float64)
-        if self.engine.__class__.__name__ == "DeviceEngine" and not host_collectives(self.dist, self.group):
-            qt = qt.to(self.engine.dev)
-        self.dist.all_reduce(qt, op=self.dist.ReduceOp.SUM, group=self.group)
+        on_device = self.engine.__class__.__name__ == "DeviceEngine" and not host_collectives(self.dist, self.group)
+        if times.size > self.fast_normalise_min and hasattr(self.engine, "quadform_fast"):
+            q = self.engine.quadform_fast(times, f_max, w) if self.rank == 0 else np.zeros(k)
+            qt = torch.tensor(q, dtype=torch.float64)
+            if on_device:
+                qt = qt.to(self.engine.dev)
+            self.dist.broadcast(qt, src=0, group=self.group)
+        else:
+            rows = balanced_triangle_rows(times.size, self.world)
+            q = np.zeros(k)
+            for k0 in range(0, k, 8):
+                q[k0:k0 + 8] = self.engine.quadform_rows(times, f_max, w[k0:k0 + 8], rows[self.rank],
+                                                         rows[self.rank + 1])
+            qt = torch.tensor(q, dtype=torch.float64)
+            if on_device:
+                qt = qt.to(self.engine.dev)
+            self.dist.all_reduce(qt, op=self.dist.ReduceOp.SUM, group=self.group)
         q = qt.cpu().numpy()
         if not np.all(q > 0):
             raise C.NumericError("gpss_interpolated: degenerate metric norm")
@@ -363,7 +386,9 @@ class SampleSplit:
     def estimate(self, x_local, power):
         """x_local: this rank's samples [s1-s0] on the device; rank 0 receives P in ``power``."""
         if self.fused:
-            self.engine.spread_slots(self.est, x_local, 0, self.s1 - self.s0, self.slot_ptrs, self.per_rank)
+            par = self.parity
+            self.parity ^= 1
+            self.engine.spread_slots(self.est, x_local, 0, self.s1 - self.s0, self.slot_ptrs[par], self.per_rank)
             if self.world > 1:  # every rank's slot stores have landed before any owner sums
                 if host_collectives(self.dist, self.group):
                     self.engine.synchronize()
@@ -371,7 +396,7 @@ class SampleSplit:
                 else:  # stream-ordered (NCCL)
                     self.dist.all_reduce(self.flag, op=self.dist.ReduceOp.SUM, group=self.group)
             count = self.per_rank * self.mr
-            self.engine.sum_slots(self.recv, self.world, count, count, self.owned)
+            self.engine.sum_slots(self.recv[par], self.world, count, count, self.owned)
         else:
             self.engine.spread(self.est, x_local, 0, self.s1 - self.s0, self.grid, self.kpad)
             self.dist.reduce_scatter_tensor(self.owned, self.grid, op=self.dist.ReduceOp.SUM, group=self.group)

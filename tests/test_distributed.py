@@ -53,11 +53,16 @@ class NumpyEngine:
         e.k = k
         e.eps = eps
         e.w = None if tapers is None else np.asarray(tapers).reshape(e.t.shape[0], k, -1)
-        if e.w is None:  # per-channel normalised tapers (ChannelShard)
-            e.w = np.stack([C.gpss_interpolated(e.t[ch], f_max, W.half_width_for(e.t[ch], 3.0), k, threads=1)[0]
+        if e.w is None:  # per-channel normalised tapers (ChannelShard), each with its own f_w
+            fw = np.broadcast_to(np.asarray(f_w, dtype=np.float64), (e.t.shape[0],))
+            e.fw = fw.copy()
+            e.w = np.stack([C.gpss_interpolated(e.t[ch], f_max, float(fw[ch]), k, threads=1)[0]
                             for ch in range(e.t.shape[0])])
         e.p, _ = C.plan_params(e.c, eps)
         return e
+
+    def quadform_fast(self, times, f_max, w):  # the O(N log N) engine call; dense here
+        return self.quadform_rows(times, f_max, w, 0, times.size)
 
     def real_dtype(self, est):
         return torch.float64
@@ -191,14 +196,22 @@ def _worker(rank, world, port, kind, q):
         wl = W.small(n=700, n_centers=256, k=3, nw=3.0, eps=1e-9, seed=5)
         eng = NumpyEngine()
         fw = float(wl.f_w[0])
-        if kind in ("sample", "sample_fused"):
+        if kind in ("sample", "sample_fused", "sample_fast_norm"):
             if kind == "sample_fused":
                 eng = SlotEngine(os.environ["NUS_TEST_SLOTDIR"], rank)
+            if kind == "sample_fast_norm":  # the N > 2^18 branch: rank 0's forms, broadcast
+                D.SampleSplit.fast_normalise_min = 100
             ss = D.SampleSplit(wl.times, wl.centers, wl.f_max, fw, 3, 1e-9, engine=eng)
             assert ss.fused == (kind == "sample_fused")
             xl = torch.as_tensor(wl.values[ss.s0:ss.s1].copy())
             pw = torch.zeros(wl.centers.size, dtype=torch.float64)
             ss.estimate(xl, pw)
+            if kind == "sample_fused":  # three more spectra: the two slot parities alternate
+                for _ in range(3):
+                    p2 = torch.zeros_like(pw)
+                    ss.estimate(xl, p2)
+                    if rank == 0:
+                        assert torch.equal(p2, pw)
             res = (pw.numpy(), ss.tapers, ss.kpad)
         elif kind == "taper":
             w, _ = C.gpss_interpolated(wl.times, wl.f_max, fw, 3, threads=1)
@@ -263,6 +276,16 @@ def test_sample_split_fused_slot_exchange_matches_single_process(tmp_path, monke
     assert rel_l2(p, ref) < 1e-12
 
 
+def test_sample_split_fast_normalisation_broadcast_matches_full():
+    """N above SampleSplit.fast_normalise_min: rank 0's forms broadcast, identical on every rank."""
+    p, tapers, kpad = _run("sample_fast_norm")
+    wl = W.small(n=700, n_centers=256, k=3, nw=3.0, eps=1e-9, seed=5)
+    w_full, _ = C.gpss_interpolated(wl.times, wl.f_max, float(wl.f_w[0]), 3, threads=1)
+    np.testing.assert_allclose(np.abs(tapers), np.abs(w_full), rtol=1e-9, atol=1e-15)
+    ref = C.mtnufft_power(wl.times, tapers, wl.values, wl.centers, 1e-9)
+    assert rel_l2(p, ref) < 1e-12
+
+
 def test_taper_shard_reduce_matches_single_process():
     p, w, _ = _run("taper")
     wl = W.small(n=700, n_centers=256, k=3, nw=3.0, eps=1e-9, seed=5)
@@ -273,8 +296,9 @@ def test_channel_shard_gather_matches_per_channel():
     p, _, _ = _run("channel")
     c3 = W.c3(channels=3, n=512)
     centers = np.arange(128) * (2500.0 / 127)
+    assert np.ptp(c3.f_w) > 0  # the channels' half-bandwidths differ: each must keep its own
     for ch in range(3):
-        w, _ = C.gpss_interpolated(c3.times[ch], 2500.0, W.half_width_for(c3.times[ch], 3.0), 2, threads=1)
+        w, _ = C.gpss_interpolated(c3.times[ch], 2500.0, float(c3.f_w[ch]), 2, threads=1)
         ref = C.mtnufft_power(c3.times[ch], w, c3.values[ch], centers, 1e-9)
         assert rel_l2(p[ch], ref) < 1e-12
 

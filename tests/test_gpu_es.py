@@ -152,8 +152,8 @@ def test_dense_clusters_wrapping_into_empty_first_segment(kern, ncl, n):
 
 @pytest.mark.parametrize("kern", ["gaussian", "es"])
 def test_random_problems_meet_the_eps_contract(kern):
-    """30 seeded random problems across the plan's regimes (Mr from 4096 to 2^17: the cuFFT and
-    the fused paths; uniform / jittered / clustered / Poisson times; wraps from < 1 to ~20;
+    """30 seeded random problems across the plan's regimes (Mr from 4096 to 2^17: single- and
+    two-pass fused FFTs; uniform / jittered / clustered / Poisson times; wraps from < 1 to ~20;
     complex y; eps from 1e-2 to 1e-12): max|fast - direct| <= eps ||y||_1 (test_nufft.cpp:81-96)."""
     rng = np.random.default_rng(2407)
     for case in range(30):

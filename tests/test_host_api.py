@@ -41,6 +41,18 @@ def test_cpp_dropin_library_exports_reference_symbols():
     del lib
 
 
+def test_library_links_no_fft_library():
+    """Every FFT of the path (and of the Radix2Fft drop-in) is the library's own kernel: the
+    shared object does not even link cuFFT (its DT_NEEDED entries)."""
+    path = os.path.join(ROOT, "paper_2407_01943_b200", "lib", "libnus_b200.so")
+    out = os.popen(f"readelf -d {path}").read()
+    needed = re.findall(r"\(NEEDED\)\s+Shared library: \[([^\]]+)\]", out)
+    assert needed, "readelf found no dynamic section"
+    assert not [n for n in needed if "cufft" in n], needed
+    syms = os.popen(f"nm -D --undefined-only {path}").read()
+    assert "cufft" not in syms
+
+
 def test_no_device_fails_loudly_without_cpu_fallback():
     try:
         info = _capi.device_info()
