@@ -342,7 +342,6 @@ def main():
     CAPI.check(L.nus_mtnufft_stage_kernels(est.h, buf, 256))
     stage_names = buf.value.decode().split(";")
     stage_bytes = [bm["spread"], bm["fft"], bm["crop"]]
-    # our own kernels only for the headline roofline (cuFFT, when it is the FFT, is a library call)
     own = [q for q in range(3) if "library" not in stage_names[q] and stage_bytes[q] > 0]
     dom_own = max(own, key=lambda q: stage_ms[q])
     traffic = None
@@ -373,7 +372,7 @@ def main():
                 "api": "nus_mtnufft_estimate_batch (host C-ABI, pinned buffers, copies overlapped across steps)"},
         "gpu_launches": int(launches),
         "gpu_launches_note": "our kernels per timed region: " + " + ".join(n for n in stage_names if "library" not in n)
-                             + " per step (a cuFFT fallback, when active, is not counted)",
+                             + " per step",
         "roofline": roof,
         "pipeline_roofline": {"bound": "hbm", "achieved": pipe_ach, "peak": peak, "unit": "GB/s",
                               "frac": pipe_ach / peak, "algorithmic_bytes_per_step": bm["total"],

@@ -43,7 +43,7 @@ enum nus_status {
   NUS_ERR_BAND_RANGE = 3,       /* nuspectral::BandRangeError */
   NUS_ERR_EXTRAPOLATION = 4,    /* nuspectral::ExtrapolationError */
   NUS_ERR_NUMERIC = 5,          /* nuspectral::Error (numeric failure) */
-  NUS_ERR_CUDA = 6,             /* CUDA / cuFFT runtime failure */
+  NUS_ERR_CUDA = 6,             /* CUDA runtime failure */
   NUS_ERR_OUT_OF_MEMORY = 7,
   NUS_ERR_NO_DEVICE = 8,
   NUS_ERR_DEGENERATE_TAPERS = 9, /* nuspectral::DegenerateTapers */

@@ -1,6 +1,6 @@
 // MtnufftEstimator on the device (src/estimators.cpp:91-122): taper setup
 // (gpss_interpolated on the GPU, or injected weights), one NUFFT plan, and the
-// per-spectrum pipeline  spread(all K) -> cuFFT -> crop+power.
+// per-spectrum pipeline  spread(all K) -> FFT pass A -> FFT pass B fused with crop+power.
 #include <algorithm>
 #include <chrono>
 #include <cmath>

@@ -598,16 +598,25 @@ void launch_tc(const SpreadParams<Real>& P, cudaStream_t s) {
   const size_t warp_bytes =
       (8 * G * kTcRows) * sizeof(double2) + (tc_pts(G) * kTcRows) * sizeof(double) + kTcRows * sizeof(int);
   const size_t smem = kMaxW2 * sizeof(double) + kTcWarps * warp_bytes;
-  static int blocks_per_sm = 0, sms = 0;
-  if (blocks_per_sm == 0) {
-    NUS_CUDA(cudaFuncSetAttribute(spread_tc_kernel<Real, XK, NS, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
-    int dev = 0;
-    NUS_CUDA(cudaGetDevice(&dev));
-    NUS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    NUS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, spread_tc_kernel<Real, XK, NS, G>,
-                                                           kTcWarps * 32, smem));
-    require(blocks_per_sm > 0, "spread: tensor-core kernel does not fit on an SM");
+  // kernel attributes are per device: configured once for every device the process uses
+  static std::mutex mu;
+  static int bps[64] = {}, sm_of[64] = {};
+  int dev = 0;
+  NUS_CUDA(cudaGetDevice(&dev));
+  require(dev < 64, "spread: device ordinal out of range");
+  int blocks_per_sm = 0, sms = 0;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (bps[dev] == 0) {
+      NUS_CUDA(cudaFuncSetAttribute(spread_tc_kernel<Real, XK, NS, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)));
+      NUS_CUDA(cudaDeviceGetAttribute(&sm_of[dev], cudaDevAttrMultiProcessorCount, dev));
+      NUS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps[dev], spread_tc_kernel<Real, XK, NS, G>,
+                                                             kTcWarps * 32, smem));
+      require(bps[dev] > 0, "spread: tensor-core kernel does not fit on an SM");
+    }
+    blocks_per_sm = bps[dev];
+    sms = sm_of[dev];
   }
   const int64_t warps = P.nseg_used * P.channels;
   const int64_t grid = std::min<int64_t>((warps + kTcWarps - 1) / kTcWarps, static_cast<int64_t>(blocks_per_sm) * sms);
@@ -668,11 +677,18 @@ template <typename Real, int KG>
 void launch_group(const SpreadParams<Real>& P, int64_t channels, cudaStream_t s) {
   const size_t smem = kBatch * KG * sizeof(typename Vec2<Real>::T) +
                       kBatch * static_cast<size_t>(P.w2 + 1) * sizeof(Real) + kBatch * sizeof(int);
-  static bool configured = false;
-  if (!configured) {
-    NUS_CUDA(cudaFuncSetAttribute(spread_gather_kernel<Real, KG>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-    configured = true;
+  static std::mutex mu;
+  static bool configured[64] = {};
+  int dev = 0;
+  NUS_CUDA(cudaGetDevice(&dev));
+  require(dev < 64, "spread: device ordinal out of range");
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!configured[dev]) {
+      NUS_CUDA(cudaFuncSetAttribute(spread_gather_kernel<Real, KG>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+      configured[dev] = true;
+    }
   }
   const dim3 grid(static_cast<unsigned>(P.ntiles), static_cast<unsigned>(channels));
   spread_gather_kernel<Real, KG><<<grid, kThreads, smem, s>>>(P);
