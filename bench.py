@@ -1,7 +1,8 @@
 #!/usr/bin/env python
 """MTNUFFT benchmark (BASELINE.json metric: NUFFT points x tapers / s, spectra/s, %HBM roofline).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c2f32|c3|c5] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c1|c2|c2f32|c3|c4|c5] [--impl ours|reference]
+                    [--shard replicas|channels|tapers|samples]
 
 One step = one multitaper spectrum estimate (spread of all K tapers -> the own two-pass FFT
 with the deconvolve/crop/eigenspectrum fused into its second pass) of one synthetic series of the workload, with
@@ -219,6 +220,163 @@ def run_reference_arm(args):
     return 0
 
 
+
+def run_sharded(args):
+    """One workload partitioned over the ranks (distributed.py), one process per GPU:
+
+    * ``--shard channels`` (C3: 256 channels x 2^18, fp32): rank r estimates channels
+      [r C/G, (r+1) C/G) with their own tapers and plans; no data-path collective.
+    * ``--shard tapers`` (C2): every rank spreads all samples for its taper subset; one NCCL
+      ``reduce`` of the I partial powers per spectrum.
+    * ``--shard samples`` (C4: N = 2^NUS_C4_LOG2N, default 26): rank r owns a contiguous sample chunk;
+      its spread stores every taper's 32-cell segments straight into the owner rank's receive slot
+      over CUDA IPC peer memory (NVLink), one stream-ordered NCCL all_reduce flag, the owners sum
+      their slots, FFT + crop their tapers, and one NCCL ``reduce`` of P.
+
+    The total work is fixed as G grows ("strong" scaling); value = all points x tapers / max over
+    ranks of the device-timed region."""
+    import torch
+    import torch.distributed as dist
+    from paper_2407_01943_b200 import _capi as CAPI
+    from paper_2407_01943_b200 import distributed as D
+    from paper_2407_01943_b200 import workloads as W
+    from paper_2407_01943_b200.api import _Estimator
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    eng = D.DeviceEngine(local)
+    stream = torch.cuda.current_stream(dev)
+    t_setup = time.perf_counter()
+    nvlink_bytes = 0
+    if args.shard == "channels":
+        total_ch = int(os.environ.get("NUS_C3_CHANNELS", "256"))
+        c0, c1 = D.split_range(total_ch, world, rank)
+        wl = W.c3(channels=c1 - c0, first_channel=c0)
+        est = _Estimator(wl.times, wl.centers, wl.f_max, wl.f_w, wl.k, wl.eps, 1, wl.precision, local)
+        xdt = torch.float32
+        x_host = np.asarray(wl.values, dtype=np.float64).reshape(c1 - c0, -1)
+        p_dev = torch.empty((c1 - c0, wl.centers.size), dtype=xdt, device=dev)
+
+        def run(x_dev):
+            eng.estimate(est, x_dev, p_dev)
+        units_rank = (c1 - c0) * wl.times.shape[-1] * wl.k
+        units_total = total_ch * wl.times.shape[-1] * wl.k
+        workload = (f"c3 channel shard: {total_ch} channels x N=2^{int(np.log2(wl.times.shape[-1]))}, "
+                    f"I=2^{int(np.log2(wl.centers.size))}, K={wl.k}, eps={wl.eps:g}, fp32, {world} rank(s)")
+        bm = est.bytes_model(0)["total"] / (c1 - c0) * total_ch
+        parallelism = f"channels split over {world} GPU(s), no data-path collective"
+    elif args.shard == "tapers":
+        wl = W.c2()
+        one = _Estimator(wl.times, wl.centers, wl.f_max, float(wl.f_w[0]), wl.k, wl.eps, 1, wl.precision, local)
+        tapers = one.tapers()[0]
+        del one
+        ts = D.TaperShard(wl.times, wl.centers, wl.f_max, float(wl.f_w[0]), tapers, wl.eps, wl.precision, engine=eng)
+        xdt = torch.float64
+        x_host = np.asarray(wl.values, dtype=np.float64).reshape(1, -1)
+        p_dev = torch.empty(wl.centers.size, dtype=xdt, device=dev)
+
+        def run(x_dev):
+            ts.estimate(x_dev[0], p_dev)
+        units_rank = wl.n * (ts.k1 - ts.k0)
+        units_total = wl.n * wl.k
+        workload = (f"c2 taper shard: N=2^20, I=2^20, K={wl.k}, eps={wl.eps:g}, fp64, {world} rank(s)")
+        bm = None
+        parallelism = f"tapers split over {world} GPU(s), NCCL reduce of I partial powers"
+    else:  # samples
+        lg = int(os.environ.get("NUS_C4_LOG2N", "26"))
+        wl = W.c4(n=1 << lg, n_centers=1 << (lg - 2))
+        ss = D.SampleSplit(wl.times, wl.centers, wl.f_max, float(wl.f_w[0]), wl.k, wl.eps, wl.precision, engine=eng)
+        xdt = torch.float64
+        x_host = np.asarray(wl.values[ss.s0:ss.s1], dtype=np.float64).reshape(1, -1)
+        p_dev = torch.empty(wl.centers.size, dtype=xdt, device=dev)
+
+        def run(x_dev):
+            ss.estimate(x_dev[0], p_dev)
+        units_rank = (ss.s1 - ss.s0) * wl.k
+        units_total = wl.n * wl.k
+        # each rank's spread stores the tapers other ranks own into their slots: (G-1)/G of K_pad grids
+        nvlink_bytes = (world - 1) * ss.per_rank * ss.mr * 16 if world > 1 else 0
+        workload = (f"c4 sample split: clustered N=2^{lg} (400 windows), I=2^{lg - 2}, K={wl.k} (NW=8), "
+                    f"eps={wl.eps:g}, fp64, {world} rank(s)")
+        bm = None
+        parallelism = (f"samples split over {world} GPU(s): spread -> peer receive slots (CUDA IPC over NVLink), "
+                       "NCCL all_reduce flag, owner slot sums, FFT + crop of owned tapers, NCCL reduce of P")
+    setup_s = time.perf_counter() - t_setup
+    x_dev = torch.tensor(x_host, dtype=xdt, device=dev)
+    for _ in range(args.warmup):
+        run(x_dev)
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    l0 = CAPI.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            run(x_dev)
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+    launches = CAPI.launch_count() - l0
+    dist.barrier()
+    ms_t = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device=dev)
+    dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    # e2e: every step copies this rank's x in from pinned host memory and its P out, in the timed region
+    e2e_steps = args.e2e_steps or max(3, min(args.steps, 20))
+    xh = torch.tensor(x_host, dtype=xdt).pin_memory()
+    ph = torch.empty(tuple(p_dev.shape), dtype=p_dev.dtype).pin_memory()
+    xd = torch.empty_like(x_dev)
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        xd.copy_(xh, non_blocking=True)
+        run(xd)
+        ph.copy_(p_dev, non_blocking=True)
+    torch.cuda.synchronize(dev)
+    e2e_t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+    dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_s = float(e2e_t.item())
+    value = units_total * args.steps / (ms_max / 1e3)
+    step_ms = ms_max / args.steps
+    peak, peak_src = load_peaks()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32" if xdt == torch.float32 else "f64", "data": "synthetic",
+        "config": {"workload": workload, "N": int(wl.times.shape[-1]), "I": int(wl.centers.size), "K": int(wl.k),
+                   "eps": wl.eps, "precision": wl.precision, "shard": args.shard},
+        "parallelism": parallelism,
+        "l2": "inputs larger than L2 (per-step grids and tables exceed 126 MB)",
+        "e2e": {"value": units_total * e2e_steps / e2e_s, "unit": UNIT,
+                "h2d_bytes_per_step": int(xh.numel() * xh.element_size()),
+                "d2h_bytes_per_step": int(ph.numel() * ph.element_size()), "steps": e2e_steps,
+                "api": "distributed.py shard estimate, torch pinned-buffer copies on the compute stream"},
+        "gpu_launches": int(launches),
+        "nvlink_bytes_per_step_per_rank": int(nvlink_bytes),
+        "units_per_step_this_rank": int(units_rank),
+        "setup_s": setup_s,
+    }
+    if bm is not None:
+        ach = bm / (step_ms / 1e3) / 1e9
+        line["roofline"] = {"bound": "hbm", "kernel": "pipeline (all ranks' algorithmic bytes / step)",
+                            "achieved": ach, "peak": peak * world, "unit": "GB/s", "frac": ach / (peak * world),
+                            "traffic": None, "peak_source": peak_src}
+    if rank == 0:
+        line["clocks"] = clk.summary()
+        print(json.dumps(line), flush=True)
+    if args.shard == "samples":
+        ss.close()
+    dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -229,10 +387,15 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--eps", type=float, default=None, help="override the workload's NUFFT tolerance")
+    ap.add_argument("--shard", default="replicas", choices=["replicas", "channels", "tapers", "samples"],
+                    help="replicas (default): an independent series per GPU; channels (C3) / tapers (C2) / "
+                         "samples (C4): one workload partitioned over the GPUs (run_sharded)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.shard != "replicas":
+        return run_sharded(args)
 
     import torch
     import torch.distributed as dist

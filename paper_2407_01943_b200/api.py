@@ -719,9 +719,12 @@ class MultiDeviceEstimator:
         c = C.f64(centers).reshape(-1)
         fw = np.ascontiguousarray(np.broadcast_to(np.atleast_1d(C.f64(f_w)).reshape(-1), (self.channels,)),
                                   dtype=np.float64)
-        devs = np.ascontiguousarray(devices, dtype=np.int32)
+        devs = np.ascontiguousarray(devices, dtype=np.int32).reshape(-1)
+        if sharding not in self.SHARDINGS:
+            raise InvalidArgument(f"MultiDeviceEstimator: unknown sharding {sharding!r}")
+        # an empty device list reaches the C-ABI, which rejects it (NUS_ERR_INVALID_ARGUMENT)
         cfg = C.MtnufftConfig(self.channels, self.n, c.size, int(k), float(f_max), float(fw[0]), float(epsilon),
-                              int(policy), _prec(precision), int(devs[0]), 0)
+                              int(policy), _prec(precision), int(devs[0]) if devs.size else 0, 0)
         tp = None if tapers is None else C.f64(tapers).reshape(self.channels, int(k), self.n)
         h = ctypes.c_void_p()
         C.check(C.lib().nus_mtnufft_multi_create(ctypes.byref(cfg), devs.ctypes.data_as(C._i32p), devs.size,

@@ -817,7 +817,7 @@ int nus_mtnufft_stage_kernels(nus_mtnufft_t est, char* out, int64_t len) {
     nus::require(est != nullptr && out != nullptr && len > 0, "stage_kernels: bad arguments");
     const char *a = nullptr, *b = nullptr;
     nus::fft_stage_names(*est->est->plan, &a, &b);
-    const std::string names = std::string(nus::spread_kernel_name()) + ";" + a + ";" + b;
+    const std::string names = nus::spread_kernel_names(*est->est->plan, est->est->cfg.k_tapers) + ";" + a + ";" + b;
     std::snprintf(out, static_cast<size_t>(len), "%s", names.c_str());
   });
 }

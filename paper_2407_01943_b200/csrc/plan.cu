@@ -171,9 +171,8 @@ __global__ void sorted_tables_kernel(const double* __restrict__ t, int64_t n, in
   // Gaussian factors around the support centre, fr' = frac - 1/2:
   //   exp(-beta (frac + w - 1 - p)^2) = A g^p C_p,  g = e^{2 beta fr'},
   //   A = e^{-beta fr' (fr' + 2w - 1)},  C_p = e^{-beta (p - w + 1/2)^2}
-  if (es) {  // ES: the spread evaluates the window polynomials at fr
-    gauss[2 * g] = static_cast<Real>(fr);
-    gauss[2 * g + 1] = Real(0);
+  if (es) {  // ES: the spread evaluates the window polynomials at fr (compact table, one real per point)
+    gauss[g] = static_cast<Real>(fr);
   } else {
   const double frc = fr - 0.5;
   gauss[2 * g] = static_cast<Real>(exp(-beta * frc * (frc + static_cast<double>(w2 - 1))));
@@ -351,6 +350,8 @@ void plan_build_tables(Plan& plan, cudaStream_t st) {
         tb.start.as<int32_t>(), p.n, p.channels, tb.nseg, p.sw, p.mr, tb.seg_range.as<int32_t>());
     note_launch();
     check_launch("seg_ranges_kernel");
+    tb.h_seg_range.resize(static_cast<size_t>(cnt) * 4);
+    NUS_CUDA(cudaMemcpyAsync(tb.h_seg_range.data(), tb.seg_range.ptr, tb.seg_range.bytes, cudaMemcpyDeviceToHost, st));
   }
   tb.deconv.alloc(p.nc * rs);
   if (p.kernel == NUS_KERNEL_ES) {

@@ -67,6 +67,9 @@ struct SpreadParams {
   const int32_t* seg_ranges;
   typename Vec2<Real>::T* const* slots;  // fused sample-split exchange (SpreadArgs::slots) or null
   int64_t per;
+  const int32_t* units;  // streaming spread: work units (SpreadTables::Units)
+  const int32_t* warp_first;  // warp w runs units [warp_first[w], warp_first[w + 1])
+  int nunits;
   int tile, w, w2, k0, kg, x_dtype, x_complex;
   Real beta, cq[kMaxW2];
   // tensor-core staging: W_{p+2} = W_p * q_p, q_{p+2} = q_p * ve (even / odd chains)
@@ -336,7 +339,7 @@ struct TcPoint {  // this lane's prefetched point of the next round: raw loads o
 // Every load is unconditional (clamped point index, clamped taper row): lanes past the
 // round's points read a real point with ti = -1, which the staging masks to x = 0; rows
 // k >= kg are read but never staged.  No lane-divergent branch, no use of loaded values.
-template <typename Real, int XK, int G>
+template <typename Real, int XK, int G, int NS>
 __device__ inline void tc_load(TcPoint<Real, G>& q, int ti, const TcCursor& u, int lane, const SpreadParams<Real>& P) {
   using R2 = typename Vec2<Real>::T;
   if (!u.valid || u.nb == 0) return;  // warp-uniform
@@ -357,7 +360,8 @@ __device__ inline void tc_load(TcPoint<Real, G>& q, int ti, const TcCursor& u, i
     q.xa = reinterpret_cast<const unsigned int*>(P.x)[xi];
   }
   q.ph = reinterpret_cast<const R2*>(P.prephase)[gi];
-  q.ag = P.gauss[gi];
+  if constexpr (NS > 0) q.ag.x = reinterpret_cast<const Real*>(P.gauss)[gi];  // ES: compact fr table
+  else q.ag = P.gauss[gi];
   const Real* tp =
       P.taper_base + (static_cast<int64_t>(u.c) * P.k_total + P.k0) * P.tstride_k + (u.b0 + j) * P.tstride_j;
   // rows k >= kg re-read row kg - 1 (never staged): the pointer stops advancing there
@@ -439,8 +443,8 @@ __global__ void __launch_bounds__(kTcWarps * 32, G == 1 ? (sizeof(Real) == 8 ? 4
   TcPoint<Real, G> pt, pt1;
   pt.ti = -1;
   pt1.ti = -1;
-  tc_load<Real, XK, G>(pt, tc_perm(cur, lane, P), cur, lane, P);
-  if constexpr (D2) tc_load<Real, XK, G>(pt1, tc_perm(n1, lane, P), n1, lane, P);
+  tc_load<Real, XK, G, NS>(pt, tc_perm(cur, lane, P), cur, lane, P);
+  if constexpr (D2) tc_load<Real, XK, G, NS>(pt1, tc_perm(n1, lane, P), n1, lane, P);
   int perm_next = tc_perm(D2 ? n2 : n1, lane, P);
 
   double cr[G][4][2], ci[G][4][2];
@@ -517,10 +521,10 @@ __global__ void __launch_bounds__(kTcWarps * 32, G == 1 ? (sizeof(Real) == 8 ? 4
     // ---- prefetch round n1 (its perm is in hand) and the perm of round n2
     if constexpr (D2) {
       pt = pt1;
-      tc_load<Real, XK, G>(pt1, perm_next, n2, lane, P);
+      tc_load<Real, XK, G, NS>(pt1, perm_next, n2, lane, P);
       perm_next = tc_perm(n3, lane, P);
     } else {
-      tc_load<Real, XK, G>(pt, perm_next, n1, lane, P);
+      tc_load<Real, XK, G, NS>(pt, perm_next, n1, lane, P);
       perm_next = tc_perm(n2, lane, P);
     }
     // ---- per block: its point range by ballot (rel ascends over the lanes), then exact
@@ -575,6 +579,315 @@ __global__ void __launch_bounds__(kTcWarps * 32, G == 1 ? (sizeof(Real) == 8 ? 4
       tc_advance(n3, pre, pp, P, stride);
     } else {
       tc_advance(n2, pre, pp, P, stride);
+    }
+  }
+  if (P.slots) __threadfence_system();  // peer-slot stores ordered before the caller's barrier
+}
+
+
+// ---- streaming FP64 tensor-core spread (default) -----------------------------------------
+// The same banded product on DMMA as spread_tc_kernel, but every warp STREAMS one contiguous
+// cell range (a work unit: equal numbers of points per warp, cut at plan time from the segment
+// point counts) instead of restaging the points of each 32-cell segment: batches of 32
+// consecutive sorted points are staged once (lane = point) and accumulated into a sliding
+// window of 64 cells (8 DMMA blocks of 8 cells x 8 tapers, accumulators in registers).  A point
+// is processed once its support [rel, rel + w2) lies inside the window; when the next point's
+// support does not, the lower 32 cells are complete (points arrive in start order), are stored,
+// and the window slides by 32 cells (upper half -> lower half, a register move).  At C2's
+// density (one point per cell, 10-cell support) this stages each point once instead of ~1.3
+// times and halves the staging rounds of the per-segment kernel (one partial batch per unit
+// instead of one per segment).  Cells without points are written as zeros by the slides.
+constexpr int kStWarps = 3;
+
+struct StUnit {  // one work unit: its cells and its point stream
+  int c, cell0, ncell;             // channel, first cell, cells
+  int wrap_lo, len0, own_lo, len;  // stream = wrapping points [wrap_lo, n) then own [own_lo, own_hi)
+};
+
+template <typename Real>
+__device__ inline StUnit st_unit(int unit, const SpreadParams<Real>& P) {
+  const int4 a = reinterpret_cast<const int4*>(P.units)[2 * unit];
+  const int4 b = reinterpret_cast<const int4*>(P.units)[2 * unit + 1];
+  StUnit u;
+  u.c = a.x;
+  u.cell0 = a.y * 32;
+  u.ncell = a.z * 32;
+  u.own_lo = a.w;
+  u.wrap_lo = b.y;
+  u.len0 = static_cast<int>(P.n) - b.y;
+  u.len = u.len0 + (b.x - a.w);
+  return u;
+}
+
+// stream position q of unit u -> sorted point index (channel-relative)
+__device__ inline int st_point(const StUnit& u, int q) { return q < u.len0 ? u.wrap_lo + q : u.own_lo + (q - u.len0); }
+
+template <typename Real, int KG>
+struct StPoint {  // this lane's prefetched point: raw loads only
+  int start, ti, q;
+  unsigned long long xa, xb;
+  typename Vec2<Real>::T ph;
+  Real fr;  // ES: fr; Gaussian: A (with g in fg)
+  Real fg;
+  Real w[KG];
+};
+
+// Loads of batch [b0, b0 + nb) of unit u (nb >= 1): every load unconditional (clamped index), so
+// no merge waits on HBM; lanes past the batch get ti = -1 (x masked to 0 at staging).
+template <typename Real, int XK, int KG, int NS>
+__device__ inline void st_load(StPoint<Real, KG>& q, int ti, const StUnit& u, int b0, int nb, int lane,
+                               const SpreadParams<Real>& P) {
+  using R2 = typename Vec2<Real>::T;
+  const bool has = lane < nb;
+  const int qq = b0 + (has ? lane : nb - 1);
+  const int pi = st_point(u, qq);
+  const int64_t base = static_cast<int64_t>(u.c) * P.n;
+  const int64_t gi = base + pi;
+  q.q = qq;
+  q.ti = has ? ti : -1;
+  const int64_t xi = base + (has ? ti : 0);
+  q.start = P.start[gi];
+  if constexpr (XK == 1) {
+    const ulonglong2 xv = reinterpret_cast<const ulonglong2*>(P.x)[xi];
+    q.xa = xv.x;
+    q.xb = xv.y;
+  } else if constexpr (XK == 0 || XK == 3) {
+    q.xa = reinterpret_cast<const unsigned long long*>(P.x)[xi];
+  } else {
+    q.xa = reinterpret_cast<const unsigned int*>(P.x)[xi];
+  }
+  q.ph = reinterpret_cast<const R2*>(P.prephase)[gi];
+  if constexpr (NS > 0) {
+    q.fr = reinterpret_cast<const Real*>(P.gauss)[gi];
+  } else {
+    const R2 ag = P.gauss[gi];
+    q.fr = ag.x;
+    q.fg = ag.y;
+  }
+  const Real* tp = P.taper_base + (static_cast<int64_t>(u.c) * P.k_total + P.k0) * P.tstride_k + pi * P.tstride_j;
+#pragma unroll
+  for (int k = 0; k < KG; ++k) q.w[k] = tp[min(k, P.kg - 1) * P.tstride_k];
+}
+
+// perm index of this lane's point of batch b0 (clamped into the stream)
+template <typename Real>
+__device__ inline int st_perm(const StUnit& u, int b0, int lane, const SpreadParams<Real>& P) {
+  const int q = min(b0 + lane, max(u.len - 1, 0));
+  return P.perm[static_cast<int64_t>(u.c) * P.n + (u.len > 0 ? st_point(u, q) : 0)];
+}
+
+// Store window blocks PH .. PH + 3 of the accumulator ring (cells `cell` .. + 31 of channel c)
+// and clear them for reuse as the window's upper half.
+template <int PH, typename Real>
+__device__ __forceinline__ void st_flush(double (&cr)[8][2], double (&ci)[8][2], int c, int cell, int g, int t,
+                                         const SpreadParams<Real>& P) {
+  using R2 = typename Vec2<Real>::T;
+  const bool k0ok = 2 * t < P.kg, k1ok = 2 * t + 1 < P.kg;
+  R2* out0;
+  R2* out1;
+  if (P.slots) {  // taper k -> owner k / per, its slot row k % per (possibly a peer GPU)
+    const int64_t ka = P.k0 + (k0ok ? 2 * t : 0), kb = P.k0 + (k1ok ? 2 * t + 1 : 0);
+    out0 = P.slots[ka / P.per] + (ka % P.per) * P.mr;
+    out1 = P.slots[kb / P.per] + (kb % P.per) * P.mr;
+  } else {
+    R2* out = P.grid + (static_cast<int64_t>(c) * P.kpad + P.k0) * P.mr;
+    out0 = out + static_cast<int64_t>(2 * t) * P.mr;
+    out1 = out0 + P.mr;
+  }
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    const int addr = cell_addr32(cell + g + 8 * b, P.blocked, P.lgC, P.lgCW, P.lgT);
+    if (k0ok) out0[addr] = R2{static_cast<Real>(cr[PH + b][0]), static_cast<Real>(ci[PH + b][0])};
+    if (k1ok) out1[addr] = R2{static_cast<Real>(cr[PH + b][1]), static_cast<Real>(ci[PH + b][1])};
+    cr[PH + b][0] = cr[PH + b][1] = ci[PH + b][0] = ci[PH + b][1] = 0.0;
+  }
+}
+
+// One accumulation pass over the staged points [pst, pend) for the 8 window blocks; window block
+// b accumulates in ring slot (b + PH) & 7.  ES (NS > 0): W rows hold zeros off the support, so
+// a = W[point][cell mod 32] needs no range test (ns <= 16 cannot alias within a block); the
+// Gaussian (NS = 0, up to 32 cells) masks by the point's rel as spread_tc_kernel does.
+template <int PH, int NS, int RS>
+__device__ __forceinline__ void st_blocks(double (&cr)[8][2], double (&ci)[8][2], int rel, int wb, int w2, int pst,
+                                          int pend, const double* sw, const double2* sz, const int* srel, int g,
+                                          int t) {
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    const int cb = wb + 8 * b;  // block's first cell
+    const int lo = max(pst, __popc(__ballot_sync(0xffffffffu, rel < cb - (w2 - 1))));
+    const int hi = min(pend, __popc(__ballot_sync(0xffffffffu, rel < cb + 8)));
+    const int S = (b + PH) & 7;  // folds to a constant: the loop is unrolled
+    if (lo < hi) {
+      // software-pipelined: the next step's operands are loaded before this step's MMAs (rows up
+      // to hi + 7 <= 39 exist and are zero or masked)
+      const double* wp = sw + (lo + t) * RS + ((8 * b) & 31) + g;
+      const double2* zp = sz + g * RS + lo + t;
+      const int* rp = srel + lo + t;
+      double a = *wp;
+      double2 zb = *zp;
+      int rl = NS == 0 ? *rp : 0;
+#pragma unroll 1
+      for (int p0 = lo;;) {
+        const double an = wp[4 * RS];
+        const double2 zn = zp[4];
+        const int rn = NS == 0 ? rp[4] : 0;
+        if constexpr (NS == 0) {
+          if (static_cast<unsigned>(cb + g - rl) >= static_cast<unsigned>(w2)) a = 0.0;
+        }
+        a = p0 + t < hi ? a : 0.0;
+        dmma_8x8x4(cr[S][0], cr[S][1], a, zb.x);
+        dmma_8x8x4(ci[S][0], ci[S][1], a, zb.y);
+        p0 += 4;
+        if (p0 >= hi) break;
+        wp += 4 * RS;
+        zp += 4;
+        rp += 4;
+        a = an;
+        zb = zn;
+        rl = rn;
+      }
+    }
+  }
+}
+
+// KG: taper rows loaded per point (8: up to 8 tapers, P.kg of them real; 1: one taper / untapered)
+template <typename Real, int XK, int NS, int KG>
+__global__ void __launch_bounds__(kStWarps * 32, 4) spread_stream_kernel(const SpreadParams<Real> P) {
+  using R2 = typename Vec2<Real>::T;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int RS = kTcRows;
+  constexpr int PTS = 40;  // 32 staged points + the pipelined 4-point steps' overrun rows (zero)
+  constexpr size_t kWarpBytes = (8 * RS) * sizeof(double2) + (PTS * RS) * sizeof(double) + PTS * sizeof(int);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  unsigned char* mine = smem_raw + warp * kWarpBytes;
+  double2* sz = reinterpret_cast<double2*>(mine);        // Z [8 tapers][RS points] (rows >= kg and columns >= 32 stay 0)
+  double* sw = reinterpret_cast<double*>(sz + 8 * RS);   // W [PTS points][RS], slot = cell mod 32 (ES: 0 off support)
+  int* srel = reinterpret_cast<int*>(sw + PTS * RS);     // rel [PTS points]
+  for (int i = lane; i < static_cast<int>((kWarpBytes - PTS * sizeof(int)) / 16); i += 32)
+    reinterpret_cast<double2*>(mine)[i] = double2{0.0, 0.0};
+  for (int i = lane; i < PTS; i += 32) srel[i] = 1 << 20;  // absent points: outside every block
+  __syncwarp();
+  pdl_launch_dependents();
+  pdl_wait();
+
+  const int w2 = NS > 0 ? NS : P.w2;
+  double cr[8][2], ci[8][2];
+#pragma unroll
+  for (int b = 0; b < 8; ++b) cr[b][0] = cr[b][1] = ci[b][0] = ci[b][1] = 0.0;
+  StPoint<Real, KG> pt;
+  const int gw = static_cast<int>(blockIdx.x) * kStWarps + warp;
+  const int unit_end = P.warp_first[gw + 1];
+  int erase_rel = 1 << 20;  // ES: support of this lane's previous point, cleared before restaging
+  for (int unit = P.warp_first[gw]; unit < unit_end; ++unit) {
+    const StUnit u = st_unit(unit, P);
+    int wb = 0;  // window base, cells relative to the unit's first cell
+    int ph = 0;  // window block b accumulates in ring slot (b + ph) & 7
+    if (u.len > 0) st_load<Real, XK, KG, NS>(pt, st_perm(u, 0, lane, P), u, 0, min(32, u.len), lane, P);
+    int perm_next = st_perm(u, 32, lane, P);
+    for (int b0 = 0; b0 < u.len; b0 += 32) {
+      // ---- stage batch [b0, b0 + nb): lane = point; z column, rel, and the W row (support only)
+      const int nb = min(32, u.len - b0);
+      const bool has = lane < nb;
+      const int rel = has ? pt.start - u.cell0 - (pt.q < u.len0 ? static_cast<int>(P.mr) : 0) : (1 << 20);
+      {
+        double xr = 0.0, xi = 0.0;
+        if constexpr (XK == 1) {
+          xr = __longlong_as_double(static_cast<long long>(pt.xa));
+          xi = __longlong_as_double(static_cast<long long>(pt.xb));
+        } else if constexpr (XK == 3) {
+          xr = __uint_as_float(static_cast<unsigned>(pt.xa));
+          xi = __uint_as_float(static_cast<unsigned>(pt.xa >> 32));
+        } else if constexpr (XK == 0) {
+          xr = __longlong_as_double(static_cast<long long>(pt.xa));
+        } else {
+          xr = __uint_as_float(static_cast<unsigned>(pt.xa));
+        }
+        if (pt.ti < P.s0 || pt.ti >= P.s1) { xr = 0.0; xi = 0.0; }  // absent lanes: ti = -1
+        const double pr = static_cast<double>(pt.ph.x), pim = static_cast<double>(pt.ph.y);
+        const double yr = xr * pr - xi * pim, yi = xr * pim + xi * pr;
+#pragma unroll
+        for (int k = 0; k < KG; ++k) {  // rows k >= kg are never written: they stay zero
+          const double wk = static_cast<double>(pt.w[k]);
+          if (KG == 1 || k < P.kg) sz[k * RS + lane] = double2{wk * yr, wk * yi};
+        }
+        srel[lane] = rel;
+        double* row = sw + lane * RS;
+        if constexpr (NS > 0) {
+          // clear the previous point's support (the rows are zero off the support), then write this one's
+#pragma unroll
+          for (int q = 0; q < NS; ++q) row[(erase_rel + q) & 31] = 0.0;
+          erase_rel = rel;
+          if (has) {
+            const double sv = 2.0 * static_cast<double>(pt.fr) - 1.0;
+            const double s2 = sv * sv;
+#pragma unroll
+            for (int q = 0; q < NS / 2; ++q) {  // even window: cells q and ns-1-q from one E/O pair
+              constexpr int D = es_degree(NS);
+              const double* cf = c_es + es_table_offset(NS) + q * (D + 1);
+              constexpr int de = D & ~1, dod = (D - 1) | 1;
+              double ev = cf[de], od = cf[dod];
+#pragma unroll
+              for (int d = de - 2; d >= 0; d -= 2) ev = fma(ev, s2, cf[d]);
+#pragma unroll
+              for (int d = dod - 2; d >= 1; d -= 2) od = fma(od, s2, cf[d]);
+              row[(rel + q) & 31] = fma(sv, od, ev);
+              row[(rel + NS - 1 - q) & 31] = fma(-sv, od, ev);
+            }
+          } else {
+            erase_rel = 0;  // nothing written: clearing slots 0 .. ns-1 next time is harmless
+          }
+        } else if (has) {  // W_p = A g^p C_p, two geometric chains (spread_tc_kernel)
+          const double gg = static_cast<double>(pt.fg), g2 = gg * gg, A = static_cast<double>(pt.fr);
+          double ae = A * P.c0, ao = A * gg * P.c1, qe = g2 * P.qe0, qo = g2 * P.qo0;
+          for (int q = 0; q < P.w2; q += 2) {
+            row[(rel + q) & 31] = ae;
+            row[(rel + q + 1) & 31] = ao;
+            ae *= qe;
+            ao *= qo;
+            qe *= P.ve;
+            qo *= P.ve;
+          }
+        }
+      }
+      __syncwarp();
+      // ---- prefetch the next batch (its perm is in hand) and the perm of the one after
+      if (b0 + 32 < u.len) {
+        st_load<Real, XK, KG, NS>(pt, perm_next, u, b0 + 32, min(32, u.len - b0 - 32), lane, P);
+        perm_next = st_perm(u, b0 + 64, lane, P);
+      }
+      // ---- accumulate the prefix of the batch whose supports fit the window; slide; repeat
+      int pst = 0;
+      for (;;) {
+        const int pend = __popc(__ballot_sync(0xffffffffu, has && rel + (w2 - 1) < wb + 64));
+        if (pend > pst) {
+          if (ph == 0) st_blocks<0, NS, RS>(cr, ci, rel, wb, w2, pst, pend, sw, sz, srel, g, t);
+          else st_blocks<4, NS, RS>(cr, ci, rel, wb, w2, pst, pend, sw, sz, srel, g, t);
+          pst = pend;
+        }
+        if (pst >= nb) break;
+        // the next point's support leaves the window: its lower 32 cells are complete
+        if (ph == 0) st_flush<0, Real>(cr, ci, u.c, u.cell0 + wb, g, t, P);
+        else st_flush<4, Real>(cr, ci, u.c, u.cell0 + wb, g, t, P);
+        ph ^= 4;
+        wb += 32;
+      }
+      __syncwarp();  // private tables are restaged next
+    }
+    // end of the unit: store the rest of its cells (zeros past the last point); leaves the ring zero
+    while (wb < u.ncell) {
+      if (ph == 0) st_flush<0, Real>(cr, ci, u.c, u.cell0 + wb, g, t, P);
+      else st_flush<4, Real>(cr, ci, u.c, u.cell0 + wb, g, t, P);
+      ph ^= 4;
+      wb += 32;
+    }
+    // the lower half now holds contributions past the unit's last cell (the upper one was cleared
+    // by the last flush): discard them
+    if (ph == 0) {
+#pragma unroll
+      for (int b = 0; b < 4; ++b) cr[b][0] = cr[b][1] = ci[b][0] = ci[b][1] = 0.0;
+    } else {
+#pragma unroll
+      for (int b = 4; b < 8; ++b) cr[b][0] = cr[b][1] = ci[b][0] = ci[b][1] = 0.0;
     }
   }
   if (P.slots) __threadfence_system();  // peer-slot stores ordered before the caller's barrier
@@ -645,7 +958,7 @@ void launch_tc_ns(const SpreadParams<Real>& P, int ns, cudaStream_t s) {
 }
 
 template <typename Real>
-void launch_tc_x(SpreadParams<Real> P, int ns, cudaStream_t s, bool two_groups = false) {
+void set_taper_base(SpreadParams<Real>& P) {
   if (P.tapers) {
     P.taper_base = P.tapers;
     P.tstride_k = P.n;
@@ -658,6 +971,11 @@ void launch_tc_x(SpreadParams<Real> P, int ns, cudaStream_t s, bool two_groups =
     P.tstride_k = 0;
     P.tstride_j = 0;
   }
+}
+
+template <typename Real>
+void launch_tc_x(SpreadParams<Real> P, int ns, cudaStream_t s, bool two_groups = false) {
+  set_taper_base(P);
   const int xk = P.x_dtype == 0 ? (P.x_complex ? 1 : 0) : (P.x_complex ? 3 : 2);
   if (two_groups) {  // real x only (the estimator's spectra)
     require(xk == 0 || xk == 2, "spread: two taper groups need real x");
@@ -670,6 +988,151 @@ void launch_tc_x(SpreadParams<Real> P, int ns, cudaStream_t s, bool two_groups =
     case 1: launch_tc_ns<Real, 1>(P, ns, s); break;
     case 2: launch_tc_ns<Real, 2>(P, ns, s); break;
     default: launch_tc_ns<Real, 3>(P, ns, s); break;
+  }
+}
+
+
+// Work units of the streaming spread: the occupied segments of all channels (each channel's in
+// the pass-A row order) weighted by the points whose start cell they hold plus a charge for their
+// cells, cut into one contiguous range of equal weight per resident warp.  A warp's range is
+// split into units where it crosses a channel boundary or the cyclic wrap of the occupied rows
+// past cell Mr - 1, so each unit's cells are consecutive; warp w runs units
+// [first[w], first[w + 1]).
+const SpreadTables::Units& stream_units(const Plan& plan, int64_t nwarps, int64_t nseg_used, int lg_spr, int row_lo,
+                                        int nrows) {
+  const SpreadTables& tb = plan.tab;
+  std::lock_guard<std::mutex> lk(tb.units_mu);
+  const int row_cnt = static_cast<int>(nseg_used >> lg_spr);
+  for (const auto& u : tb.units)
+    if (u.nwarps == nwarps && u.row_lo == row_lo && u.row_cnt == row_cnt) return u;
+  const int64_t C = plan.p.channels, nseg = tb.nseg;
+  const int32_t* hs = tb.h_seg_range.data();
+  require(static_cast<int64_t>(tb.h_seg_range.size()) == C * nseg * 4, "spread: segment ranges missing");
+  constexpr int64_t kSegCharge = 2;  // ~ the cost of two points: one slide + store of 32 cells
+  auto abs_seg = [&](int64_t u) {
+    const int64_t row = ((u >> lg_spr) + row_lo) & (nrows - 1);
+    return (row << lg_spr) | (u & ((int64_t{1} << lg_spr) - 1));
+  };
+  // cumulative weight over (channel, used segment)
+  const int64_t total_segs = C * nseg_used;
+  std::vector<int64_t> cum(static_cast<size_t>(total_segs) + 1, 0);
+  for (int64_t c = 0; c < C; ++c) {
+    const int32_t* h = hs + c * nseg * 4;
+    for (int64_t u = 0; u < nseg_used; ++u) {
+      const int64_t a = abs_seg(u);
+      const int64_t own = h[4 * a + 1] - (a > 0 ? h[4 * (a - 1) + 1] : 0);
+      const int64_t gidx = c * nseg_used + u;
+      cum[gidx + 1] = cum[gidx] + own + kSegCharge;
+    }
+  }
+  const int64_t total = cum[total_segs];
+  std::vector<int32_t> units, first(static_cast<size_t>(nwarps) + 1, 0);
+  int64_t g0 = 0;
+  for (int64_t w = 0; w < nwarps; ++w) {
+    first[w] = static_cast<int32_t>(units.size() / 8);
+    int64_t g1 = total_segs;
+    if (w + 1 < nwarps) {
+      const int64_t target = static_cast<int64_t>((static_cast<__int128>(total) * (w + 1)) / nwarps);
+      g1 = std::lower_bound(cum.begin() + g0, cum.end(), target) - cum.begin();
+      g1 = std::min(std::max(g1, g0), total_segs);
+    }
+    // pieces of [g0, g1): cut at channel boundaries and at the cyclic wrap (absolute segment 0)
+    for (int64_t lo = g0; lo < g1;) {
+      const int64_t c = lo / nseg_used;
+      int64_t hi = std::min(g1, (c + 1) * nseg_used);
+      for (int64_t q = lo + 1; q < hi; ++q)
+        if (abs_seg(q - c * nseg_used) == 0) { hi = q; break; }
+      const int32_t* h = hs + c * nseg * 4;
+      const int64_t a0 = abs_seg(lo - c * nseg_used), na = hi - lo;
+      units.insert(units.end(), {static_cast<int32_t>(c), static_cast<int32_t>(a0), static_cast<int32_t>(na),
+                                 h[4 * a0], h[4 * (a0 + na - 1) + 1], h[4 * a0 + 2], 0, 0});
+      lo = hi;
+    }
+    g0 = g1;
+  }
+  first[nwarps] = static_cast<int32_t>(units.size() / 8);
+  SpreadTables::Units nu;
+  nu.nwarps = nwarps;
+  nu.row_lo = row_lo;
+  nu.row_cnt = row_cnt;
+  nu.count = static_cast<int64_t>(units.size() / 8);
+  std::vector<int32_t> all(units);
+  all.insert(all.end(), first.begin(), first.end());
+  nu.buf.alloc(all.size() * sizeof(int32_t));
+  NUS_CUDA(cudaMemcpy(nu.buf.ptr, all.data(), all.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+  tb.units.push_back(std::move(nu));
+  return tb.units.back();
+}
+
+template <typename Real, int XK, int NS, int KG>
+void launch_stream(SpreadParams<Real> P, const Plan& plan, cudaStream_t s) {
+  const size_t smem = kStWarps * ((8 * kTcRows) * sizeof(double2) + (40 * kTcRows) * sizeof(double) +
+                                  40 * sizeof(int));
+  static std::mutex mu;
+  static int bps[64] = {}, sm_of[64] = {};
+  int dev = 0;
+  NUS_CUDA(cudaGetDevice(&dev));
+  require(dev < 64, "spread: device ordinal out of range");
+  int blocks_per_sm = 0, sms = 0;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (bps[dev] == 0) {
+      NUS_CUDA(cudaFuncSetAttribute(spread_stream_kernel<Real, XK, NS, KG>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      NUS_CUDA(cudaDeviceGetAttribute(&sm_of[dev], cudaDevAttrMultiProcessorCount, dev));
+      NUS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps[dev], spread_stream_kernel<Real, XK, NS, KG>,
+                                                             kStWarps * 32, smem));
+      require(bps[dev] > 0, "spread: streaming kernel does not fit on an SM");
+    }
+    blocks_per_sm = bps[dev];
+    sms = sm_of[dev];
+  }
+  const int64_t grid = static_cast<int64_t>(blocks_per_sm) * sms;
+  const auto& units = stream_units(plan, grid * kStWarps, P.nseg_used, P.lg_spr, P.row_lo, P.nrows);
+  P.units = static_cast<const int32_t*>(units.buf.ptr);
+  P.nunits = static_cast<int>(units.count);
+  P.warp_first = P.units + 8 * units.count;
+  if constexpr (NS > 0) es_upload();
+  launch_pdl(spread_stream_kernel<Real, XK, NS, KG>, dim3(static_cast<unsigned>(grid)), dim3(kStWarps * 32), smem, s,
+             P);
+  note_launch();
+  check_launch("spread_stream_kernel");
+}
+
+template <typename Real, int XK, int KG>
+void launch_stream_ns(const SpreadParams<Real>& P, const Plan& plan, int ns, cudaStream_t s) {
+  switch (ns) {
+    case 0: launch_stream<Real, XK, 0, KG>(P, plan, s); break;
+    case 4: launch_stream<Real, XK, 4, KG>(P, plan, s); break;
+    case 6: launch_stream<Real, XK, 6, KG>(P, plan, s); break;
+    case 8: launch_stream<Real, XK, 8, KG>(P, plan, s); break;
+    case 10: launch_stream<Real, XK, 10, KG>(P, plan, s); break;
+    case 12: launch_stream<Real, XK, 12, KG>(P, plan, s); break;
+    case 14: launch_stream<Real, XK, 14, KG>(P, plan, s); break;
+    case 16: launch_stream<Real, XK, 16, KG>(P, plan, s); break;
+    default: fail(NUS_ERR_INVALID_ARGUMENT, "spread: unsupported ES width");
+  }
+}
+
+// one taper group (kg <= 8) on the streaming kernel
+template <typename Real>
+void launch_stream_x(SpreadParams<Real> P, const Plan& plan, int ns, cudaStream_t s) {
+  set_taper_base(P);
+  const int xk = P.x_dtype == 0 ? (P.x_complex ? 1 : 0) : (P.x_complex ? 3 : 2);
+  if (P.kg == 1) {
+    switch (xk) {
+      case 0: launch_stream_ns<Real, 0, 1>(P, plan, ns, s); break;
+      case 1: launch_stream_ns<Real, 1, 1>(P, plan, ns, s); break;
+      case 2: launch_stream_ns<Real, 2, 1>(P, plan, ns, s); break;
+      default: launch_stream_ns<Real, 3, 1>(P, plan, ns, s); break;
+    }
+    return;
+  }
+  switch (xk) {  // complex x with tapers: the O(N log N) normalisation's lattice chunks (normalise.cu)
+    case 0: launch_stream_ns<Real, 0, 8>(P, plan, ns, s); break;
+    case 1: launch_stream_ns<Real, 1, 8>(P, plan, ns, s); break;
+    case 2: launch_stream_ns<Real, 2, 8>(P, plan, ns, s); break;
+    default: launch_stream_ns<Real, 3, 8>(P, plan, ns, s); break;
   }
 }
 
@@ -694,6 +1157,69 @@ void launch_group(const SpreadParams<Real>& P, int64_t channels, cudaStream_t s)
   spread_gather_kernel<Real, KG><<<grid, kThreads, smem, s>>>(P);
   note_launch();
   check_launch("spread_gather_kernel");
+}
+
+
+struct SpreadLaunch {
+  enum Kind { kStream, kSegment, kSegment2, kGather } kind;
+  int64_t k0, kg;
+};
+
+// Which spread kernel(s) a spectrum of k tapers launches, and their taper ranges.
+//   spread_stream_kernel (default): one launch per group of <= 8 tapers, balanced;
+//   spread_tc_kernel with two taper groups per staging: 9..16 tapers of a real series on dense data
+//     (C3, C4), NUS_SPREAD_GROUPS=1 turns it off;
+//   NUS_SPREAD=segment: the per-segment spread_tc_kernel for single groups; NUS_SPREAD=gather: the
+//   CUDA-core broadcast gather (Gaussian only), which also takes Gaussians wider than 32 cells.
+std::vector<SpreadLaunch> spread_schedule(const Plan& plan, int64_t k, bool x_complex, bool slots) {
+  const PlanParams& p = plan.p;
+  static const bool use_tc = [] {
+    const char* e = std::getenv("NUS_SPREAD");
+    return !(e && std::strcmp(e, "gather") == 0);
+  }();
+  static const bool use_stream = [] {
+    const char* e = std::getenv("NUS_SPREAD");
+    return !(e && (std::strcmp(e, "gather") == 0 || std::strcmp(e, "segment") == 0));
+  }();
+  require(use_tc || p.kernel == NUS_KERNEL_GAUSSIAN, "spread: the gather kernel implements the Gaussian only");
+  // the tensor-core kernels' weight rows hold one 32-cell window: wider Gaussians (eps < ~2e-13,
+  // 2w > 32) take the gather kernel; the ES window is at most 16 cells
+  const bool tc = use_tc && p.sw <= 32;
+  require(!slots || tc, "spread: slot output needs the tensor-core kernel");
+  static const bool two_ok = [] {
+    const char* e = std::getenv("NUS_SPREAD_GROUPS");
+    return !(e && std::strcmp(e, "1") == 0);
+  }();
+  // two groups per staging: C3 (fp32, K = 9, ns = 6) 781 vs 1085 us against two per-segment
+  // single-group launches, C4's structure 543 vs 623 us; slower with the narrowest window (ns = 4)
+  // unless the data is dense
+  static const int64_t dense_min = [] {
+    const char* e = std::getenv("NUS_SPREAD_DENSE_MIN");
+    return e ? static_cast<int64_t>(std::atoll(e)) : int64_t{48};
+  }();
+  const FusedFft& f = plan.ffft;
+  const int64_t nseg_used = (f.ready && f.blocked) ? static_cast<int64_t>(f.row_cnt) << (f.lgC - 5) : plan.tab.nseg;
+  const bool dense = p.n >= dense_min * nseg_used || p.sw >= 6;
+  const SpreadLaunch::Kind single = !tc ? SpreadLaunch::kGather : use_stream ? SpreadLaunch::kStream : SpreadLaunch::kSegment;
+  std::vector<SpreadLaunch> out;
+  if (tc && two_ok && dense && k > 8 && !x_complex) {  // launches of <= 16 tapers, balanced
+    const int64_t launches = (k + 15) / 16;
+    int64_t kb = 0;
+    for (int64_t li = 0; li < launches; ++li) {
+      const int64_t kn = (k - kb + (launches - li) - 1) / (launches - li);
+      out.push_back({kn > 8 ? SpreadLaunch::kSegment2 : single, kb, kn});
+      kb += kn;
+    }
+    return out;
+  }
+  const int64_t groups = (k + 7) / 8;  // taper groups of at most 8, balanced
+  int64_t k0 = 0;
+  for (int64_t gi = 0; gi < groups; ++gi) {
+    const int64_t kg = (k - k0 + (groups - gi) - 1) / (groups - gi);
+    out.push_back({single, k0, kg});
+    k0 += kg;
+  }
+  return out;
 }
 
 template <typename Real>
@@ -763,68 +1289,27 @@ void spread_typed(const Plan& plan, const SpreadArgs& a, cudaStream_t s) {
     P.qo0 = std::exp(-4.0 * p.beta * (2.5 - static_cast<double>(p.w)));  // C_3 / C_1
     P.ve = std::exp(-8.0 * p.beta);
   }
-  // NUS_SPREAD=gather selects the CUDA-core broadcast gather (kept for comparison)
-  static const bool use_tc = [] {
-    const char* e = std::getenv("NUS_SPREAD");
-    return !(e && std::strcmp(e, "gather") == 0);
-  }();
-  require(use_tc || p.kernel == NUS_KERNEL_GAUSSIAN, "spread: the gather kernel implements the Gaussian only");
-  // the tensor-core kernel's weight rows hold one 32-cell window: wider Gaussians (eps < ~2e-13,
-  // 2w > 32) take the gather kernel; the ES window is at most 16 cells
-  const bool tc = use_tc && p.sw <= 32;
-  require(!a.slots || tc, "spread: slot output needs the tensor-core kernel");
   const int ns = p.kernel == NUS_KERNEL_ES ? p.sw : 0;
-  const int64_t k = a.tapers ? a.k : 1;
-  // 9..16 tapers of a real series: both groups from one staging of the points
-  static const bool two_ok = [] {  // NUS_SPREAD_GROUPS=1 turns it off, see below
-    const char* e = std::getenv("NUS_SPREAD_GROUPS");
-    return !(e && std::strcmp(e, "1") == 0);
-  }();
-  // Two groups per staging (4 CTAs / SM with 32-row weight tables) against two single-group
-  // launches: C3 (fp32, K = 9, ns = 6) 781 vs 1085 us, C4's structure (dense) 543 vs 623 us,
-  // C5 (K = 15 / 31, fp64, ns >= 8) 4-8 % faster; slower only with the narrowest window (ns = 4,
-  // eps >= 1e-4: up to 18 % in fp32 on C5), which keeps single groups unless the data is dense.
-  static const int64_t dense_min = [] {
-    const char* e = std::getenv("NUS_SPREAD_DENSE_MIN");
-    return e ? static_cast<int64_t>(std::atoll(e)) : int64_t{48};
-  }();
-  const bool dense = p.n >= dense_min * P.nseg_used || p.sw >= 6;
-  if (tc && two_ok && dense && k > 8 && !a.x_complex) {  // launches of <= 16 tapers, balanced
-    const int64_t launches = (k + 15) / 16;
-    int64_t kb = 0;
-    for (int64_t li = 0; li < launches; ++li) {
-      const int64_t kn = (k - kb + (launches - li) - 1) / (launches - li);
-      P.k0 = static_cast<int>(kb);
-      P.kg = static_cast<int>(kn);
-      if (kn > 8) launch_tc_x<Real>(P, ns, s, true);
-      else launch_tc_x<Real>(P, ns, s);
-      kb += kn;
+  const auto sched = spread_schedule(plan, a.tapers ? a.k : 1, a.x_complex, a.slots != nullptr);
+  for (const SpreadLaunch& l : sched) {
+    P.k0 = static_cast<int>(l.k0);
+    P.kg = static_cast<int>(l.kg);
+    switch (l.kind) {
+      case SpreadLaunch::kStream: launch_stream_x<Real>(P, plan, ns, s); break;
+      case SpreadLaunch::kSegment: launch_tc_x<Real>(P, ns, s); break;
+      case SpreadLaunch::kSegment2: launch_tc_x<Real>(P, ns, s, true); break;
+      default:
+        switch (l.kg) {
+          case 1: launch_group<Real, 1>(P, p.channels, s); break;
+          case 2: launch_group<Real, 2>(P, p.channels, s); break;
+          case 3: launch_group<Real, 3>(P, p.channels, s); break;
+          case 4: launch_group<Real, 4>(P, p.channels, s); break;
+          case 5: launch_group<Real, 5>(P, p.channels, s); break;
+          case 6: launch_group<Real, 6>(P, p.channels, s); break;
+          case 7: launch_group<Real, 7>(P, p.channels, s); break;
+          default: launch_group<Real, 8>(P, p.channels, s); break;
+        }
     }
-    return;
-  }
-  // taper groups of at most 8, balanced
-  const int64_t groups = (k + 7) / 8;
-  int64_t k0 = 0;
-  for (int64_t gidx = 0; gidx < groups; ++gidx) {
-    const int64_t kg = (k - k0 + (groups - gidx) - 1) / (groups - gidx);
-    P.k0 = static_cast<int>(k0);
-    P.kg = static_cast<int>(kg);
-    if (tc) {
-      launch_tc_x<Real>(P, ns, s);
-      k0 += kg;
-      continue;
-    }
-    switch (kg) {
-      case 1: launch_group<Real, 1>(P, p.channels, s); break;
-      case 2: launch_group<Real, 2>(P, p.channels, s); break;
-      case 3: launch_group<Real, 3>(P, p.channels, s); break;
-      case 4: launch_group<Real, 4>(P, p.channels, s); break;
-      case 5: launch_group<Real, 5>(P, p.channels, s); break;
-      case 6: launch_group<Real, 6>(P, p.channels, s); break;
-      case 7: launch_group<Real, 7>(P, p.channels, s); break;
-      default: launch_group<Real, 8>(P, p.channels, s); break;
-    }
-    k0 += kg;
   }
 }
 
@@ -832,7 +1317,20 @@ void spread_typed(const Plan& plan, const SpreadArgs& a, cudaStream_t s) {
 
 const char* spread_kernel_name() {
   const char* e = std::getenv("NUS_SPREAD");
-  return (e && std::strcmp(e, "gather") == 0) ? "spread_gather_kernel" : "spread_tc_kernel";
+  return (e && std::strcmp(e, "gather") == 0) ? "spread_gather_kernel"
+         : (e && std::strcmp(e, "segment") == 0) ? "spread_tc_kernel"
+                                                 : "spread_stream_kernel";
+}
+
+std::string spread_kernel_names(const Plan& plan, int64_t k) {
+  std::string names;
+  for (const SpreadLaunch& l : spread_schedule(plan, k, false, false)) {
+    const char* n = l.kind == SpreadLaunch::kStream ? "spread_stream_kernel"
+                    : l.kind == SpreadLaunch::kGather ? "spread_gather_kernel"
+                                                      : "spread_tc_kernel";
+    if (names.find(n) == std::string::npos) names += (names.empty() ? "" : "+") + std::string(n);
+  }
+  return names;
 }
 
 namespace {
