@@ -59,7 +59,7 @@ def make_workload(name, rank):
     if name == "c3":
         return W.c3(channels=int(os.environ.get("NUS_C3_CHANNELS", "32")), first_channel=32 * rank)
     if name == "c5":
-        return W.c5()
+        return W.c5(k=int(os.environ.get("NUS_C5_K", "7")))
     if name == "c4":  # C4's structure; N defaults to 2^22 (DPSS setup at 2^26)
         lg = int(os.environ.get("NUS_C4_LOG2N", "22"))
         return W.c4(n=1 << lg, n_centers=1 << (lg - 2))

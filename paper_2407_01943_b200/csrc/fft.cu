@@ -746,194 +746,6 @@ __global__ void __launch_bounds__(kFftThreads * kGroups, 1) fft_rows_crop_async_
 }
 
 
-// ---- fused pass A -> pass B per taper, the pass-A output resident in L2 ------------------
-// One persistent launch per spectrum (C = 2048-point rows, 64 <= R <= 2048).  Work items, taken
-// in order from an atomic dispenser:
-//   block m = 0 .. Q + S - 2:   A(m): the nA column tiles of grid q = m (if m < Q),
-//                               then B(m - S + 1): its R / 2 row pairs (if m >= S - 1),
-// q = channel * K + taper.  A(q) writes q's column FFTs (inter-pass twiddle applied) into scratch
-// slot q mod S; B(q) transforms the rows of that slot and adds d^2 |X|^2 / divisor of the crop's
-// bins to P.  S slots of Mr complex (2 x 33.5 MB at C2) fit the 126 MB L2, so the pass-A output
-// does not make the HBM round trip of the two-kernel path.  Dependencies, on device-scope
-// counters that only grow (launch e waits for e-based targets; nothing is reset per launch):
-//   a row pair of B(q) waits for A(q)'s nA tiles;  A(q), q >= S, waits for B(q - S)'s R/2 pairs
-//   (slot reuse);  B(c, k, row) adds into P after B(c, k - 1, row) (k-ordered sums: deterministic).
-// An item only waits for items dispensed before it, which are held by running CTAs: no deadlock
-// whatever the residency.  Scratch and P are read with ld.global.cg (L2), never from a stale L1.
-template <typename Real, typename PReal>
-struct FusedArgs {
-  using T2 = typename C2<Real>::T;
-  const T2* grid;
-  T2* scratch;       // [S][Mr]
-  int64_t mr;
-  int R, C, CW, kk, kpad, Q, S, nA, nB;  // kk = tapers per channel
-  const T2 *tw_r, *tw_hi, *tw_lo, *tw_c;
-  int lo_bits, row_lo, row_cnt;
-  const Real* deconv;
-  int64_t nc, mode_offset;
-  T2* j_out;
-  PReal* power;
-  double divisor;
-  int accumulate;
-  unsigned long long* ctr;  // [0] dispenser, [1, 1 + Q) doneA, [1 + Q, 1 + 2Q) doneB, then rowdone[C][R]
-  unsigned long long epoch, total;
-};
-
-__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void spin_until(const unsigned long long* p, unsigned long long target) {
-  while (ld_acquire_u64(p) < target) __nanosleep(64);
-}
-
-template <typename Real, typename PReal, int R0A, int LGR, int R0B>
-__global__ void __launch_bounds__(kFftThreads, 2) fft_fused_kernel(const FusedArgs<Real, PReal> a) {
-  using T2 = typename C2<Real>::T;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T2* const buf = reinterpret_cast<T2*>(smem_raw);  // pass A: [R][CW]; pass B: two rows of C
-  __shared__ long long s_item;
-  constexpr int NT = kFftThreads;
-  constexpr int R = 1 << LGR;
-  constexpr int lgCW = 12 - LGR, CW = 1 << lgCW;
-  constexpr int lgC = 11;  // C = 2048: 128 threads x 16 registers per row
-  constexpr int NTB = 128;
-  const int tid = threadIdx.x;
-  const int nblk = a.C >> lgCW;  // column tiles per grid (= nA)
-  unsigned long long* const doneA = a.ctr + 1;
-  unsigned long long* const doneB = a.ctr + 1 + a.Q;
-  unsigned long long* const rowdone = a.ctr + 1 + 2 * a.Q;
-  const unsigned long long base = a.epoch * (a.total + gridDim.x);
-  const int blk_a = a.nA, blk_b = a.nB;  // items per A / B part of a block
-  for (;;) {
-    if (tid == 0) s_item = static_cast<long long>(atomicAdd(a.ctr, 1ull) - base);
-    __syncthreads();
-    const long long item = s_item;
-    __syncthreads();
-    if (item >= static_cast<long long>(a.total)) break;
-    // decode: blocks 0 .. S-2 hold nA items, S-1 .. Q-1 nA + nB, Q .. Q+S-2 nB
-    int m, idx;
-    bool is_a;
-    {
-      const long long pre = static_cast<long long>(a.S - 1) * blk_a;
-      if (item < pre) {
-        m = static_cast<int>(item / blk_a);
-        idx = static_cast<int>(item - static_cast<long long>(m) * blk_a);
-        is_a = true;
-      } else {
-        const long long mid = static_cast<long long>(a.Q - a.S + 1) * (blk_a + blk_b);
-        const long long r = item - pre;
-        if (r < mid) {
-          const int mb = static_cast<int>(r / (blk_a + blk_b));
-          const int off = static_cast<int>(r - static_cast<long long>(mb) * (blk_a + blk_b));
-          m = a.S - 1 + mb;
-          is_a = off < blk_a;
-          idx = is_a ? off : off - blk_a;
-        } else {
-          const long long r2 = r - mid;
-          m = a.Q + static_cast<int>(r2 / blk_b);
-          idx = static_cast<int>(r2 - static_cast<long long>(m - a.Q) * blk_b);
-          is_a = false;
-        }
-      }
-    }
-    if (is_a) {
-      // ---- A(q = m), column tile idx: fft_cols_blk_kernel's body into slot q mod S
-      const int q = m;
-      if (q >= a.S && tid == 0) spin_until(doneB + (q - a.S), (a.epoch + 1) * static_cast<unsigned long long>(blk_b));
-      __syncthreads();
-      const int ch = q / a.kk, kq = q - ch * a.kk;
-      const T2* src = a.grid + (static_cast<int64_t>(ch) * a.kpad + kq) * a.mr + (static_cast<int64_t>(idx) << (LGR + lgCW));
-      T2 v[16];
-#pragma unroll
-      for (int sl = 0; sl < 16; ++sl) {
-        int f, e;
-        stage0_index<R0A, NT>(sl, LGR, lgCW, f, e);
-        const bool occ = static_cast<unsigned>((e - a.row_lo) & (R - 1)) < static_cast<unsigned>(a.row_cnt);
-        v[sl] = occ ? src[e * CW + f] : T2{Real(0), Real(0)};
-      }
-      int f, out0, st;
-      fft16_regs<R0A, false, T2, NT>(v, buf, LGR, lgCW, CW, 1, a.tw_r, f, out0, st);
-      T2* g = a.scratch + static_cast<int64_t>(q % a.S) * a.mr;
-      const int j2 = idx * CW + f;
-      const PassATwiddles<T2> tw2 = pass_a_twiddles(static_cast<int64_t>(j2), out0, st, a.mr, a.lo_bits, a.tw_hi, a.tw_lo);
-      T2 w = cmul(tw2.b_hi, tw2.b_lo);
-      const T2 wstep = cmul(tw2.s_hi, tw2.s_lo);
-      T2* gr = g + j2 + static_cast<int64_t>(out0) * a.C;
-      const int64_t rstep = static_cast<int64_t>(st) * a.C;
-#pragma unroll
-      for (int qq = 0; qq < 16; ++qq) {
-        gr[qq * rstep] = cmul(v[qq], w);
-        if (qq < 15) w = cmul(w, wstep);
-      }
-      __threadfence();  // this thread's stores visible device-wide before the tile counts as done
-      __syncthreads();  // (buf free for the next item too)
-      if (tid == 0) atomicAdd(doneA + q, 1ull);
-    } else {
-      // ---- B(q = m - S + 1), row pair idx: rows 2 idx + grp, 128 threads each
-      const int q = m - a.S + 1;
-      if (tid == 0) spin_until(doneA + q, (a.epoch + 1) * static_cast<unsigned long long>(blk_a));
-      __syncthreads();
-      const int grp = tid >> 7, gt = tid & (NTB - 1);
-      const int k1 = 2 * idx + grp;
-      const int ch = q / a.kk, kq = q - ch * a.kk;
-      const T2* row = a.scratch + static_cast<int64_t>(q % a.S) * a.mr + static_cast<int64_t>(k1) * a.C;
-      T2 v[16];
-#pragma unroll
-      for (int sl = 0; sl < 16; ++sl) {
-        int ff, e;
-        stage0_index<R0B, NTB>(sl, lgC, 0, ff, e, gt);
-        v[sl] = __ldcg(row + e);
-      }
-      int f = 0, out0 = 0, step = 1;
-      fft16_regs<R0B, true, T2, NTB>(v, buf + grp * 2048, lgC, 0, 1, 2048, a.tw_c, f, out0, step, 1 + grp, gt);
-      // crop (nufft.cpp:131-140): bin kb = k1 + R k2 keeps i = m + I/2, (-m) mod Mr = kb
-      int64_t iv[kCropN];
-      Real dv[kCropN];
-#pragma unroll
-      for (int c = 0; c < kCropN; ++c) {
-        const int64_t kb = static_cast<int64_t>(k1) + static_cast<int64_t>(R) * (out0 + crop_q(c) * step);
-        int64_t ii = -1;
-        if (kb <= a.mode_offset) ii = a.mode_offset - kb;
-        else if (a.mr - kb < a.nc - a.mode_offset) ii = a.mode_offset + (a.mr - kb);
-        iv[c] = ii;
-        dv[c] = a.deconv[ii < 0 ? 0 : (ii < a.nc ? ii : a.nc - 1)];
-      }
-      if (a.j_out) {
-#pragma unroll
-        for (int c = 0; c < kCropN; ++c) {
-          const int64_t ii = iv[c];
-          const T2 x = v[crop_q(c)];
-          if (ii >= 0 && ii < a.nc) a.j_out[(static_cast<int64_t>(ch) * a.kk + kq) * a.nc + ii] = T2{dv[c] * x.x, dv[c] * x.y};
-        }
-      }
-      unsigned long long* rd = rowdone + static_cast<int64_t>(ch) * R + k1;
-      // P of this row: after taper kq - 1's sums (launch e: rowdone = e K + kq)
-      if (gt == 0) spin_until(rd, a.epoch * static_cast<unsigned long long>(a.kk) + kq);
-      group_bar<NTB>(1 + grp);
-      if (a.power) {
-#pragma unroll
-        for (int c = 0; c < kCropN; ++c) {
-          const int64_t ii = iv[c];
-          if (ii >= 0 && ii < a.nc) {
-            const T2 x = v[crop_q(c)];
-            const double d = static_cast<double>(dv[c]);
-            const PReal val = static_cast<PReal>(d * d * static_cast<double>(x.x * x.x + x.y * x.y) / a.divisor);
-            PReal* dst = a.power + static_cast<int64_t>(ch) * a.nc + ii;
-            *dst = (kq > 0 || a.accumulate) ? __ldcg(dst) + val : val;
-          }
-        }
-      }
-      __threadfence();  // this row's P stores visible before the next taper of the row reads them
-      group_bar<NTB>(1 + grp);
-      if (gt == 0) atomicAdd(rd, 1ull);
-      __syncthreads();  // both rows done (buf free; the slot's rows read)
-      if (tid == 0) atomicAdd(doneB + q, 1ull);
-    }
-  }
-}
-
 template <typename Real>
 __global__ void twiddle_table_kernel(typename C2<Real>::T* __restrict__ out, int64_t count, int64_t stride,
                                      int64_t denom) {
@@ -993,11 +805,6 @@ void configure_fft_kernels() {
   NUS_ATTR((fft_cols_blk_kernel<double, 4, kFftThreads, 10>));
   NUS_ATTR((fft_cols_blk_kernel<double, 8, kFftThreads, 11>));
   NUS_ATTR((fft_cols_blk_kernel<double, 16, kFftThreads, 12>));
-#define NUS_ATTRF(RL, PR, L) NUS_ATTR((fft_fused_kernel<RL, PR, (L % 4 == 0) ? 16 : (1 << (L % 4)), L, 8>))
-#define NUS_ATTRF3(L) NUS_ATTRF(double, double, L); NUS_ATTRF(float, float, L); NUS_ATTRF(float, double, L)
-  NUS_ATTRF3(6); NUS_ATTRF3(7); NUS_ATTRF3(8); NUS_ATTRF3(9); NUS_ATTRF3(10); NUS_ATTRF3(11);
-#undef NUS_ATTRF3
-#undef NUS_ATTRF
 #undef NUS_ATTR
   const int smem_w = 2 * kFftElems * static_cast<int>(sizeof(double2));
 #define NUS_ATTRW(KERN) NUS_CUDA(cudaFuncSetAttribute(KERN, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_w))
@@ -1233,11 +1040,6 @@ bool fused_pass_b_async() {
 }
 
 void fft_stage_names(const Plan& plan, const char** a, const char** b) {
-  if (fused_ab_supported(plan)) {
-    *a = "fft_fused_kernel";
-    *b = "(fused: pass B + crop in fft_fused_kernel)";
-    return;
-  }
   if (!plan.ffft.ready) {
     *a = "stockham_r2_kernel";
     *b = "crop_power_kernel";
@@ -1292,109 +1094,6 @@ void fft_generic_inplace(void* data, int64_t n, int64_t batch, bool f64, bool in
   NUS_CUDA(cudaStreamSynchronize(s));  // scratch is released at scope end
 }
 
-
-// Fused pass A -> pass B (fft_fused_kernel) for C = 2048 rows and 64 <= R <= 2048, register pass A;
-// NUS_FFT_FUSED=0 keeps the two-kernel path.
-bool fused_ab_supported(const Plan& plan) {
-  const char* e = std::getenv("NUS_FFT_FUSED");  // read per call: tests compare both paths in one process
-  const bool off = e && std::strcmp(e, "0") == 0;
-  const FusedFft& f = plan.ffft;
-  return !off && f.ready && f.blocked && f.C == 2048 && f.R >= 64 && f.R <= 2048 && f.cols_mode == 1 &&
-         !fused_pass_b_async();
-}
-
-namespace {
-
-template <typename Real, typename PReal, int LGR>
-void launch_fused_ab_r(const FusedArgs<Real, PReal>& a, int grid, cudaStream_t s) {
-  constexpr int R0A = (LGR % 4 == 0) ? 16 : (1 << (LGR % 4));
-  auto kern = fft_fused_kernel<Real, PReal, R0A, LGR, 8>;
-  const size_t smem = static_cast<size_t>(kFftElems) * sizeof(typename C2<Real>::T);
-  kern<<<static_cast<unsigned>(grid), kFftThreads, smem, s>>>(a);
-}
-
-template <typename Real, typename PReal>
-void launch_fused_ab(Plan& plan, void* grid, int64_t k, int64_t kpad, void* j_out, void* power, double divisor,
-                     bool accumulate, cudaStream_t s) {
-  const PlanParams& p = plan.p;
-  FusedFft& f = plan.ffft;
-  using T2 = typename C2<Real>::T;
-  const int Q = static_cast<int>(p.channels * k);
-  const size_t slot = static_cast<size_t>(p.mr) * sizeof(T2);
-  // slots: as many as ~80 MB of L2 holds (at least 2, at most Q)
-  const int S = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(Q, std::max<int64_t>(2, (80ll << 20) / slot))));
-  if (f.scratch.bytes < S * slot) {
-    NUS_CUDA(cudaStreamSynchronize(s));
-    f.scratch.alloc(S * slot);
-  }
-  const int lgR = ilog2(f.R);
-  const int nA = f.C / f.CW, nB = f.R / 2;
-  const size_t nctr = 1 + 2 * static_cast<size_t>(Q) + static_cast<size_t>(p.channels) * f.R;
-  const unsigned long long total = static_cast<unsigned long long>(Q) * (nA + nB);
-  // persistent (2 CTAs / SM); the dispenser needs no co-residency, this only sizes the launch
-  const int grid_n = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(total), 2ll * sm_count()));
-  if (f.fused_q != Q || f.fused_grid != grid_n || f.fused_ctr.bytes < nctr * 8) {  // fresh counters, epoch 0
-    NUS_CUDA(cudaStreamSynchronize(s));
-    if (f.fused_ctr.bytes < nctr * 8) f.fused_ctr.alloc(nctr * 8);
-    NUS_CUDA(cudaMemsetAsync(f.fused_ctr.ptr, 0, f.fused_ctr.bytes, s));
-    f.fused_q = Q;
-    f.fused_grid = grid_n;
-    f.fused_epoch = 0;
-  }
-  FusedArgs<Real, PReal> a{};
-  a.grid = static_cast<const T2*>(grid);
-  a.scratch = f.scratch.as<T2>();
-  a.mr = p.mr;
-  a.R = f.R;
-  a.C = f.C;
-  a.CW = f.CW;
-  a.kk = static_cast<int>(k);
-  a.kpad = static_cast<int>(kpad);
-  a.Q = Q;
-  a.S = S;
-  a.nA = nA;
-  a.nB = nB;
-  a.tw_r = f.tw_r.as<T2>();
-  a.tw_hi = f.tw_hi.as<T2>();
-  a.tw_lo = f.tw_lo.as<T2>();
-  a.tw_c = f.tw_c.as<T2>();
-  a.lo_bits = f.lo_bits;
-  a.row_lo = f.row_lo;
-  a.row_cnt = f.row_cnt;
-  a.deconv = plan.tab.deconv.as<Real>();
-  a.nc = p.nc;
-  a.mode_offset = p.mode_offset;
-  a.j_out = static_cast<T2*>(j_out);
-  a.power = static_cast<PReal*>(power);
-  a.divisor = divisor;
-  a.accumulate = accumulate ? 1 : 0;
-  a.ctr = f.fused_ctr.as<unsigned long long>();
-  a.epoch = f.fused_epoch++;
-  a.total = total;
-  switch (lgR) {
-    case 6: launch_fused_ab_r<Real, PReal, 6>(a, grid_n, s); break;
-    case 7: launch_fused_ab_r<Real, PReal, 7>(a, grid_n, s); break;
-    case 8: launch_fused_ab_r<Real, PReal, 8>(a, grid_n, s); break;
-    case 9: launch_fused_ab_r<Real, PReal, 9>(a, grid_n, s); break;
-    case 10: launch_fused_ab_r<Real, PReal, 10>(a, grid_n, s); break;
-    case 11: launch_fused_ab_r<Real, PReal, 11>(a, grid_n, s); break;
-    default: fail(NUS_ERR_INVALID_ARGUMENT, "fft: fused pass A+B column length");
-  }
-  note_launch();
-  check_launch("fft_fused_kernel");
-}
-
-}  // namespace
-
-void run_fused_ab(Plan& plan, void* grid, int64_t k, int64_t kpad, void* j_out, void* power, bool power_f64,
-                  double divisor, bool accumulate, cudaStream_t s) {
-  if (plan.p.precision == NUS_F64)
-    launch_fused_ab<double, double>(plan, grid, k, kpad, j_out, power, divisor, accumulate, s);
-  else if (power_f64)
-    launch_fused_ab<float, double>(plan, grid, k, kpad, j_out, power, divisor, accumulate, s);
-  else
-    launch_fused_ab<float, float>(plan, grid, k, kpad, j_out, power, divisor, accumulate, s);
-}
 
 void run_fused_pass_a(Plan& plan, void* grid, int64_t k, int64_t kpad, cudaStream_t s) {
   if (plan.ffft.R <= 1) return;

@@ -153,14 +153,9 @@ void estimator_run(Estimator& est, const void* x_dev, int x_dtype, void* power_d
     if (timed) NUS_CUDA(cudaEventRecord(ev[0], s));
     launch_spread(plan, a, s);
     if (timed) NUS_CUDA(cudaEventRecord(ev[1], s));
-    if (fused_ab_supported(plan)) {  // pass A + pass B/crop/power in one kernel (stage 3 empty)
-      run_fused_ab(plan, est.grid.ptr, K, K, j_dev, power_dev, power_f64, static_cast<double>(K), false, s);
-      if (timed) NUS_CUDA(cudaEventRecord(ev[2], s));
-    } else {
-      run_fft(plan, est.grid.ptr, K, K, s);
-      if (timed) NUS_CUDA(cudaEventRecord(ev[2], s));
-      run_crop(plan, est.grid.ptr, K, K, j_dev, power_dev, power_f64, static_cast<double>(K), false, s);
-    }
+    run_fft(plan, est.grid.ptr, K, K, s);
+    if (timed) NUS_CUDA(cudaEventRecord(ev[2], s));
+    run_crop(plan, est.grid.ptr, K, K, j_dev, power_dev, power_f64, static_cast<double>(K), false, s);
     if (timed) {
       NUS_CUDA(cudaEventRecord(ev[3], s));
       ++est.tslot;
@@ -325,13 +320,8 @@ void estimator_bytes(const Estimator& est, int x_dtype, double* total, double* s
   const double b_crop = K * I * c + I * r;
   // per-stage figures are what each launched kernel must move: with the fused FFT the
   // crop/power epilogue lives in pass B, which reads the K rows-transformed grids once
-  double b_stage3 = est.plan->ffft.ready ? K * Mr * c + I * r : b_crop;
-  double b_stage2 = est.plan->ffft.ready && est.plan->ffft.R <= 1 ? 0.0 : b_fft;
-  if (fused_ab_supported(*est.plan)) {
-    // one kernel: reads the K grids from HBM, writes P; the pass-A output stays in L2
-    b_stage2 = K * Mr * c + I * r;
-    b_stage3 = 0.0;
-  }
+  const double b_stage3 = est.plan->ffft.ready ? K * Mr * c + I * r : b_crop;
+  const double b_stage2 = est.plan->ffft.ready && est.plan->ffft.R <= 1 ? 0.0 : b_fft;
   if (spread) *spread = C * b_spread;
   if (fft) *fft = C * b_stage2;
   if (crop) *crop = C * b_stage3;

@@ -6,6 +6,7 @@
 
 #include <atomic>
 #include <cstdint>
+#include <deque>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
@@ -129,11 +130,11 @@ struct SpreadTables {
   // Work units of the streaming spread (spread.cu): contiguous cell ranges of equal work, one per
   // resident warp; built on first use per (warps, occupied rows) and cached.
   struct Units {
-    int64_t nwarps = 0, count = 0;
+    int64_t nwarps = 0, count = 0, ilv = 0;
     int row_lo = 0, row_cnt = 0;
     DeviceBuffer buf;             // int32 [count][8]: channel, first segment, segments, own lo, own hi, wrap lo, 0, 0
   };
-  mutable std::vector<Units> units;
+  mutable std::deque<Units> units;  // deque: references stay valid as entries are added
   mutable std::mutex units_mu;
   DeviceBuffer tile_range;      // int32 [C][ntiles+1][2]: point range of tile (lo, hi)
   DeviceBuffer wrap_lo;         // int32 [C]: first sorted point whose support wraps into tile 0
@@ -159,12 +160,6 @@ struct FusedFft {
   int row_lo = 0, row_cnt = 1;
   DeviceBuffer tw_r, tw_c, tw_hi, tw_lo;
   DeviceBuffer zeros;  // 16 KB of zeros (bulk-copy source)
-  // fused pass A -> pass B (fft_fused_kernel): device counters (dispenser, per-grid and per-row
-  // completion) that only grow; launch `fused_epoch` waits for epoch-based targets.  Reset when the
-  // grid count Q or the launch size changes.
-  DeviceBuffer fused_ctr;
-  int fused_q = -1, fused_grid = 0;
-  unsigned long long fused_epoch = 0;
 };
 
 struct Plan {
@@ -239,11 +234,6 @@ const char* spread_kernel_name();
 void fft_stage_names(const Plan& plan, const char** pass_a, const char** pass_b);
 void fused_fft_prepare(Plan& plan);
 void run_fused_pass_a(Plan& plan, void* grid, int64_t k, int64_t kpad, cudaStream_t s);
-// Pass A and pass B + crop/power of all K grids in one persistent kernel with the pass-A output
-// held in L2 (fft.cu fft_fused_kernel); supported for 2048-point rows and 64 <= R <= 2048.
-bool fused_ab_supported(const Plan& plan);
-void run_fused_ab(Plan& plan, void* grid, int64_t k, int64_t kpad, void* j_out, void* power, bool power_f64,
-                  double divisor, bool accumulate, cudaStream_t s);
 // Spread kernel(s) a spectrum of k tapers launches (bench / tests)
 std::string spread_kernel_names(const Plan& plan, int64_t k);
 void run_fused_pass_b(Plan& plan, void* grid, int64_t k, int64_t kpad, void* j_out, void* power, bool power_f64,

@@ -646,7 +646,6 @@ __device__ inline void st_load(StPoint<Real, KG>& q, int ti, const StUnit& u, in
   q.q = qq;
   q.ti = has ? ti : -1;
   const int64_t xi = base + (has ? ti : 0);
-  q.start = P.start[gi];
   if constexpr (XK == 1) {
     const ulonglong2 xv = reinterpret_cast<const ulonglong2*>(P.x)[xi];
     q.xa = xv.x;
@@ -656,6 +655,7 @@ __device__ inline void st_load(StPoint<Real, KG>& q, int ti, const StUnit& u, in
   } else {
     q.xa = reinterpret_cast<const unsigned int*>(P.x)[xi];
   }
+  q.start = P.start[gi];
   q.ph = reinterpret_cast<const R2*>(P.prephase)[gi];
   if constexpr (NS > 0) {
     q.fr = reinterpret_cast<const Real*>(P.gauss)[gi];
@@ -703,50 +703,51 @@ __device__ __forceinline__ void st_flush(double (&cr)[8][2], double (&ci)[8][2],
   }
 }
 
-// One accumulation pass over the staged points [pst, pend) for the 8 window blocks; window block
-// b accumulates in ring slot (b + PH) & 7.  ES (NS > 0): W rows hold zeros off the support, so
-// a = W[point][cell mod 32] needs no range test (ns <= 16 cannot alias within a block); the
-// Gaussian (NS = 0, up to 32 cells) masks by the point's rel as spread_tc_kernel does.
-template <int PH, int NS, int RS>
-__device__ __forceinline__ void st_blocks(double (&cr)[8][2], double (&ci)[8][2], int rel, int wb, int w2, int pst,
-                                          int pend, const double* sw, const double2* sz, const int* srel, int g,
-                                          int t) {
+// One accumulation pass over the staged points [pst, pend) for the 8 window blocks (block b in
+// registers cr[b], ci[b]).  Per block its point range [lo, hi) comes from two ballots (rel ascends
+// over the lanes), then exact 4-point steps on the tensor cores.  ES (NS > 0): the W rows are zero
+// off the point's support and an ns <= 16 support cannot alias a block cell mod 32 for a point of
+// [lo, hi), so a = W[point][cell mod 32] as stored, masked only past hi; the Gaussian (NS = 0, up
+// to 32 cells, rows not cleared) also masks cells outside the point's support.
+template <int NS, int RS, int PTS>
+__device__ __forceinline__ void st_pass(double (&cr)[8][2], double (&ci)[8][2], int rel, int wb, int w2, int pst,
+                                        int pend, const double* sw, const double2* sz, const int* srel, int g,
+                                        int t) {
+  const double* wrow = sw + g;            // + point row * RS + slot base
+  const double2* zcol = sz + g * RS + t;  // + p0
+  const int* rcol = srel + t;
 #pragma unroll
   for (int b = 0; b < 8; ++b) {
     const int cb = wb + 8 * b;  // block's first cell
     const int lo = max(pst, __popc(__ballot_sync(0xffffffffu, rel < cb - (w2 - 1))));
     const int hi = min(pend, __popc(__ballot_sync(0xffffffffu, rel < cb + 8)));
-    const int S = (b + PH) & 7;  // folds to a constant: the loop is unrolled
-    if (lo < hi) {
-      // software-pipelined: the next step's operands are loaded before this step's MMAs (rows up
-      // to hi + 7 <= 39 exist and are zero or masked)
-      const double* wp = sw + (lo + t) * RS + ((8 * b) & 31) + g;
-      const double2* zp = sz + g * RS + lo + t;
-      const int* rp = srel + lo + t;
-      double a = *wp;
-      double2 zb = *zp;
-      int rl = NS == 0 ? *rp : 0;
-#pragma unroll 1
-      for (int p0 = lo;;) {
-        const double an = wp[4 * RS];
-        const double2 zn = zp[4];
-        const int rn = NS == 0 ? rp[4] : 0;
-        if constexpr (NS == 0) {
-          if (static_cast<unsigned>(cb + g - rl) >= static_cast<unsigned>(w2)) a = 0.0;
-        }
-        a = p0 + t < hi ? a : 0.0;
-        dmma_8x8x4(cr[S][0], cr[S][1], a, zb.x);
-        dmma_8x8x4(ci[S][0], ci[S][1], a, zb.y);
-        p0 += 4;
-        if (p0 >= hi) break;
-        wp += 4 * RS;
-        zp += 4;
-        rp += 4;
-        a = an;
-        zb = zn;
-        rl = rn;
-      }
+    for (int p0 = lo; p0 < hi; p0 += 4) {
+      const int pi = p0 + t;  // rows up to hi + 3 <= 34 < PTS: the overrun rows are zero
+      double a = wrow[pi * RS + ((8 * b) & 31)];
+      bool keep = pi < hi;
+      if constexpr (NS == 0) keep = keep && static_cast<unsigned>(cb + g - rcol[p0]) < static_cast<unsigned>(w2);
+      a = keep ? a : 0.0;
+      const double2 zb = zcol[p0];
+      dmma_8x8x4(cr[b][0], cr[b][1], a, zb.x);
+      dmma_8x8x4(ci[b][0], ci[b][1], a, zb.y);
     }
+  }
+  (void)PTS;
+}
+
+// Store the window's lower 32 cells (blocks 0..3, cells `cell` .. + 31 of channel c), then slide:
+// the upper half becomes the lower one and the upper half restarts at zero.
+template <typename Real>
+__device__ __forceinline__ void st_flush_slide(double (&cr)[8][2], double (&ci)[8][2], int c, int cell, int g, int t,
+                                               const SpreadParams<Real>& P) {
+  st_flush<0, Real>(cr, ci, c, cell, g, t, P);
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    cr[b][0] = cr[b + 4][0];
+    cr[b][1] = cr[b + 4][1];
+    ci[b][0] = ci[b + 4][0];
+    ci[b][1] = ci[b + 4][1];
+    cr[b + 4][0] = cr[b + 4][1] = ci[b + 4][0] = ci[b + 4][1] = 0.0;
   }
 }
 
@@ -756,16 +757,17 @@ __global__ void __launch_bounds__(kStWarps * 32, 4) spread_stream_kernel(const S
   using R2 = typename Vec2<Real>::T;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int RS = kTcRows;
-  constexpr int PTS = 40;  // 32 staged points + the pipelined 4-point steps' overrun rows (zero)
-  constexpr size_t kWarpBytes = (8 * RS) * sizeof(double2) + (PTS * RS) * sizeof(double) + PTS * sizeof(int);
+  constexpr int PTS = 35;  // 32 staged points + the last 4-point step's overrun rows (zero)
+  constexpr int RELS = (PTS + 3) & ~3;  // rel entries, rounded so every warp's tables stay 16-byte aligned
+  constexpr size_t kWarpBytes = (8 * RS) * sizeof(double2) + (PTS * RS) * sizeof(double) + RELS * sizeof(int);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   unsigned char* mine = smem_raw + warp * kWarpBytes;
   double2* sz = reinterpret_cast<double2*>(mine);        // Z [8 tapers][RS points] (rows >= kg and columns >= 32 stay 0)
   double* sw = reinterpret_cast<double*>(sz + 8 * RS);   // W [PTS points][RS], slot = cell mod 32 (ES: 0 off support)
   int* srel = reinterpret_cast<int*>(sw + PTS * RS);     // rel [PTS points]
-  for (int i = lane; i < static_cast<int>((kWarpBytes - PTS * sizeof(int)) / 16); i += 32)
+  for (int i = lane; i < static_cast<int>((kWarpBytes - RELS * sizeof(int)) / 16); i += 32)
     reinterpret_cast<double2*>(mine)[i] = double2{0.0, 0.0};
-  for (int i = lane; i < PTS; i += 32) srel[i] = 1 << 20;  // absent points: outside every block
+  for (int i = lane; i < RELS; i += 32) srel[i] = 1 << 20;  // absent points: outside every block
   __syncwarp();
   pdl_launch_dependents();
   pdl_wait();
@@ -781,7 +783,6 @@ __global__ void __launch_bounds__(kStWarps * 32, 4) spread_stream_kernel(const S
   for (int unit = P.warp_first[gw]; unit < unit_end; ++unit) {
     const StUnit u = st_unit(unit, P);
     int wb = 0;  // window base, cells relative to the unit's first cell
-    int ph = 0;  // window block b accumulates in ring slot (b + ph) & 7
     if (u.len > 0) st_load<Real, XK, KG, NS>(pt, st_perm(u, 0, lane, P), u, 0, min(32, u.len), lane, P);
     int perm_next = st_perm(u, 32, lane, P);
     for (int b0 = 0; b0 < u.len; b0 += 32) {
@@ -855,40 +856,30 @@ __global__ void __launch_bounds__(kStWarps * 32, 4) spread_stream_kernel(const S
         st_load<Real, XK, KG, NS>(pt, perm_next, u, b0 + 32, min(32, u.len - b0 - 32), lane, P);
         perm_next = st_perm(u, b0 + 64, lane, P);
       }
-      // ---- accumulate the prefix of the batch whose supports fit the window; slide; repeat
+      // ---- accumulate the prefix of the batch whose supports fit the window; when the next point's
+      // support leaves it, the lower 32 cells are complete (points arrive in start order): store
+      // them, slide the window by 32 cells, repeat
       int pst = 0;
       for (;;) {
         const int pend = __popc(__ballot_sync(0xffffffffu, has && rel + (w2 - 1) < wb + 64));
         if (pend > pst) {
-          if (ph == 0) st_blocks<0, NS, RS>(cr, ci, rel, wb, w2, pst, pend, sw, sz, srel, g, t);
-          else st_blocks<4, NS, RS>(cr, ci, rel, wb, w2, pst, pend, sw, sz, srel, g, t);
+          st_pass<NS, RS, PTS>(cr, ci, rel, wb, w2, pst, pend, sw, sz, srel, g, t);
           pst = pend;
         }
         if (pst >= nb) break;
-        // the next point's support leaves the window: its lower 32 cells are complete
-        if (ph == 0) st_flush<0, Real>(cr, ci, u.c, u.cell0 + wb, g, t, P);
-        else st_flush<4, Real>(cr, ci, u.c, u.cell0 + wb, g, t, P);
-        ph ^= 4;
+        st_flush_slide<Real>(cr, ci, u.c, u.cell0 + wb, g, t, P);
         wb += 32;
       }
       __syncwarp();  // private tables are restaged next
     }
-    // end of the unit: store the rest of its cells (zeros past the last point); leaves the ring zero
+    // end of the unit: store the rest of its cells (zeros past the last point)
     while (wb < u.ncell) {
-      if (ph == 0) st_flush<0, Real>(cr, ci, u.c, u.cell0 + wb, g, t, P);
-      else st_flush<4, Real>(cr, ci, u.c, u.cell0 + wb, g, t, P);
-      ph ^= 4;
+      st_flush_slide<Real>(cr, ci, u.c, u.cell0 + wb, g, t, P);
       wb += 32;
     }
-    // the lower half now holds contributions past the unit's last cell (the upper one was cleared
-    // by the last flush): discard them
-    if (ph == 0) {
+    // the lower half now holds contributions past the unit's last cell: discard them
 #pragma unroll
-      for (int b = 0; b < 4; ++b) cr[b][0] = cr[b][1] = ci[b][0] = ci[b][1] = 0.0;
-    } else {
-#pragma unroll
-      for (int b = 4; b < 8; ++b) cr[b][0] = cr[b][1] = ci[b][0] = ci[b][1] = 0.0;
-    }
+    for (int b = 0; b < 4; ++b) cr[b][0] = cr[b][1] = ci[b][0] = ci[b][1] = 0.0;
   }
   if (P.slots) __threadfence_system();  // peer-slot stores ordered before the caller's barrier
 }
@@ -1003,9 +994,23 @@ const SpreadTables::Units& stream_units(const Plan& plan, int64_t nwarps, int64_
   const SpreadTables& tb = plan.tab;
   std::lock_guard<std::mutex> lk(tb.units_mu);
   const int row_cnt = static_cast<int>(nseg_used >> lg_spr);
-  for (const auto& u : tb.units)
-    if (u.nwarps == nwarps && u.row_lo == row_lo && u.row_cnt == row_cnt) return u;
   const int64_t C = plan.p.channels, nseg = tb.nseg;
+  // nparts = nwarps * ilv equal-weight parts; part j runs on warp j mod nwarps, so with ilv > 1 the
+  // parts in flight at any time are neighbours in memory.  Measured (K = 7, fp64): C2 (2^20 points,
+  // point tables ~100 MB, largely L2-resident across spectra) is fastest with one part per warp
+  // (87.4 us; 2 parts 90.1, 4 parts 94.9); C5 (2^22 points, ~370 MB of tables streamed from HBM)
+  // with ~300 points per part (1/2/4/8/16/32 parts per warp: 471/431/381/329/339/394 us; the
+  // per-segment kernel 386 us): the DRAM pages of the neighbouring parts are then open together.
+  // NUS_SPREAD_ILV overrides.
+  const int64_t total_points = C * plan.p.n;
+  const int64_t ilv = [&] {
+    const char* e = std::getenv("NUS_SPREAD_ILV");
+    if (e) return std::max<int64_t>(1, std::atoll(e));
+    if (total_points <= (int64_t{1} << 21)) return int64_t{1};
+    return std::min<int64_t>(32, std::max<int64_t>(1, (total_points / nwarps + 150) / 300));
+  }();
+  for (const auto& u : tb.units)
+    if (u.nwarps == nwarps && u.ilv == ilv && u.row_lo == row_lo && u.row_cnt == row_cnt) return u;
   const int32_t* hs = tb.h_seg_range.data();
   require(static_cast<int64_t>(tb.h_seg_range.size()) == C * nseg * 4, "spread: segment ranges missing");
   constexpr int64_t kSegCharge = 2;  // ~ the cost of two points: one slide + store of 32 cells
@@ -1026,13 +1031,14 @@ const SpreadTables::Units& stream_units(const Plan& plan, int64_t nwarps, int64_
     }
   }
   const int64_t total = cum[total_segs];
-  std::vector<int32_t> units, first(static_cast<size_t>(nwarps) + 1, 0);
+  const int64_t nparts = nwarps * ilv;
+  std::vector<std::vector<int32_t>> parts(static_cast<size_t>(nparts));
   int64_t g0 = 0;
-  for (int64_t w = 0; w < nwarps; ++w) {
-    first[w] = static_cast<int32_t>(units.size() / 8);
+  for (int64_t w = 0; w < nparts; ++w) {
+    std::vector<int32_t>& units = parts[w];
     int64_t g1 = total_segs;
-    if (w + 1 < nwarps) {
-      const int64_t target = static_cast<int64_t>((static_cast<__int128>(total) * (w + 1)) / nwarps);
+    if (w + 1 < nparts) {
+      const int64_t target = static_cast<int64_t>((static_cast<__int128>(total) * (w + 1)) / nparts);
       g1 = std::lower_bound(cum.begin() + g0, cum.end(), target) - cum.begin();
       g1 = std::min(std::max(g1, g0), total_segs);
     }
@@ -1050,9 +1056,18 @@ const SpreadTables::Units& stream_units(const Plan& plan, int64_t nwarps, int64_
     }
     g0 = g1;
   }
+  std::vector<int32_t> units, first(static_cast<size_t>(nwarps) + 1, 0);
+  for (int64_t w = 0; w < nwarps; ++w) {
+    first[w] = static_cast<int32_t>(units.size() / 8);
+    for (int64_t j = 0; j < ilv; ++j) {
+      const std::vector<int32_t>& pu = parts[j * nwarps + w];
+      units.insert(units.end(), pu.begin(), pu.end());
+    }
+  }
   first[nwarps] = static_cast<int32_t>(units.size() / 8);
   SpreadTables::Units nu;
   nu.nwarps = nwarps;
+  nu.ilv = ilv;
   nu.row_lo = row_lo;
   nu.row_cnt = row_cnt;
   nu.count = static_cast<int64_t>(units.size() / 8);
@@ -1066,8 +1081,8 @@ const SpreadTables::Units& stream_units(const Plan& plan, int64_t nwarps, int64_
 
 template <typename Real, int XK, int NS, int KG>
 void launch_stream(SpreadParams<Real> P, const Plan& plan, cudaStream_t s) {
-  const size_t smem = kStWarps * ((8 * kTcRows) * sizeof(double2) + (40 * kTcRows) * sizeof(double) +
-                                  40 * sizeof(int));
+  const size_t smem = kStWarps * ((8 * kTcRows) * sizeof(double2) + (35 * kTcRows) * sizeof(double) +
+                                  36 * sizeof(int));  // = kStWarps * kWarpBytes of the kernel
   static std::mutex mu;
   static int bps[64] = {}, sm_of[64] = {};
   int dev = 0;
@@ -1364,6 +1379,7 @@ void sum_slots(const void* base, int64_t nslots, int64_t slot_stride, int64_t co
   note_launch();
   check_launch("sum_slots_kernel");
 }
+
 
 void launch_spread(const Plan& plan, const SpreadArgs& a, cudaStream_t s) {
   if (plan.p.precision == NUS_F64)

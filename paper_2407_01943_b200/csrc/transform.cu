@@ -93,10 +93,6 @@ void run_crop(Plan& plan, void* grid, int64_t k, int64_t kpad, void* j_out, void
 
 void run_transform(Plan& plan, void* grid, int64_t k, int64_t kpad, void* j_out, void* power,
                    bool power_f64, double divisor, bool accumulate, cudaStream_t s) {
-  if (fused_ab_supported(plan)) {
-    run_fused_ab(plan, grid, k, kpad, j_out, power, power_f64, divisor, accumulate, s);
-    return;
-  }
   run_fft(plan, grid, k, kpad, s);
   run_crop(plan, grid, k, kpad, j_out, power, power_f64, divisor, accumulate, s);
 }

@@ -104,12 +104,9 @@ def test_estimator_power_at_every_fused_row_length(lg_mr, precision):
     assert est.info.mr == mr
     names = est.stage_kernels()
     assert names[0] == "spread_stream_kernel"
-    if 1 << 17 <= mr <= 1 << 22:  # 2048-point rows: pass A and pass B + crop in one persistent kernel
-        assert names[1] == "fft_fused_kernel" and names[2].startswith("(fused")
-    else:
-        assert names[2] == "fft_rows_crop_kernel"
-        assert names[1] == ("(none: single pass)" if mr <= 8192 else
-                            "fft_cols_small_kernel" if mr <= 1 << 15 else "fft_cols_blk_kernel")
+    assert names[2] == "fft_rows_crop_kernel"
+    assert names[1] == ("(none: single pass)" if mr <= 8192 else
+                        "fft_cols_small_kernel" if mr <= 1 << 15 else "fft_cols_blk_kernel")
     p = est.power(x)
     tol = 1e-10 if precision == "f64" else 1e-4
     for ch in range(chans):
@@ -154,37 +151,3 @@ def test_largest_grids_own_fft(lg_mr, monkeypatch):
         gen = nus.NufftPlan(nus.SamplingGrid(t), c, 1e-9, FAST).execute(y)
         assert rel_l2(got, gen) < 1e-12
 
-
-@pytest.mark.parametrize("lg_mr", [17, 18, 19, 20, 21, 22])
-@pytest.mark.parametrize("precision", ["f64", "f32"])
-def test_fused_pass_ab_matches_two_kernel_path(lg_mr, precision, monkeypatch):
-    """fft_fused_kernel (pass A -> pass B per grid, the pass-A output in L2 slots, P summed in taper
-    order behind per-row counters) against the two-kernel path (NUS_FFT_FUSED=0) on the same plan:
-    P and J of several channels, two consecutive spectra (counters carried across launches), and P
-    against the C restatement of the reference."""
-    mr = 1 << lg_mr
-    nc = mr // 2
-    rng = np.random.default_rng(300 + lg_mr)
-    chans, n, k = 2, 6000, 5
-    ts = np.stack([np.sort(rng.uniform(0, 40, n)) + 1e-9 * np.arange(n) for _ in range(chans)])
-    c = (1.7 / 40.0) * np.arange(nc)
-    w = rng.uniform(0.5, 1.5, (chans, k, n)) / np.sqrt(n)
-    eps = 1e-9 if precision == "f64" else 1e-5
-    est = nus.api._Estimator(ts, c, 10.0, 0.1, k, eps, 1, precision, 0, tapers=w)
-    assert est.info.mr == mr
-    assert est.stage_kernels()[1] == "fft_fused_kernel"
-    xs = [rng.standard_normal((chans, n)) for _ in range(3)]
-    p_f = [est.power(x) for x in xs]
-    j_f = est.eigencoefficients(xs[0])
-    monkeypatch.setenv("NUS_FFT_FUSED", "0")
-    p_2 = [est.power(x) for x in xs]
-    j_2 = est.eigencoefficients(xs[0])
-    monkeypatch.delenv("NUS_FFT_FUSED")
-    p_again = est.power(xs[1])
-    tol = 1e-13 if precision == "f64" else 1e-6
-    for a, b in zip(p_f, p_2):
-        assert rel_l2(a, b) < tol
-    assert rel_l2(j_f, j_2) < tol
-    assert np.array_equal(p_again, p_f[1])  # deterministic: k-ordered sums
-    ref = C.mtnufft_power(ts[1], w[1], xs[2][1], c, eps)
-    assert rel_l2(p_f[2][1], ref) < (1e-10 if precision == "f64" else 1e-4)

@@ -70,7 +70,7 @@ def test_c3_256x2e18_channels_fp32_vs_reference(kern):
     wl = W.c3(channels=256)
     est = nus.api._Estimator(wl.times, wl.centers, wl.f_max, wl.f_w, wl.k, wl.eps, 1, "f32", 0)
     assert est.info.mr == 1 << 18
-    assert est.stage_kernels()[:2] == ["spread_tc_kernel", "fft_fused_kernel"]  # K = 9: two taper groups
+    assert est.stage_kernels() == ["spread_tc_kernel", "fft_cols_blk_kernel", "fft_rows_crop_kernel"]  # K = 9: two taper groups
     p = est.power(wl.values)
     w = est.tapers()
 
