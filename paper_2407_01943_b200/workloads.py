@@ -2,9 +2,13 @@
 
 No public dataset is involved (the paper's impedance data is proprietary);
 these generators follow the shapes, sizes and value distributions that
-BASELINE.json states for each config.  They use numpy's
-PCG64 with seed = 20240702 + config index (+ channel), so every run, the GPU
-path and the CPU oracle see identical inputs.
+BASELINE.json states for each config.  Every draw comes from
+the reference's own generator (``Rng`` of src/simkit.cpp:19-57: SplitMix64,
+uniform = (u64 >> 11) 2^-53 rejecting 0, polar Box-Muller with a cached spare),
+consumed in bulk by :class:`RefRng` -- bit-identical to calling the reference's
+next_uniform / next_gauss in the same order -- with one substream per config
+and channel, ``Rng::substream(Rng::substream(20240702, config), channel)``
+(SURVEY §8(d)); the reference's own tooling regenerates the same inputs.
 
 Conventions shared by all configs:
   * f_w = NW / (h N) with h = span / (N - 1), so the reference's
@@ -22,6 +26,105 @@ import numpy as np
 from scipy.signal import lfilter
 
 BASE_SEED = 20240702
+_GAMMA = np.uint64(0x9E3779B97F4A7C15)
+
+
+def _mix64(z: np.ndarray) -> np.ndarray:
+    with np.errstate(over="ignore"):
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return z ^ (z >> np.uint64(31))
+
+
+def substream(seed: int, key: int) -> int:
+    """Rng::substream (simkit.cpp:50-56): one SplitMix64 scramble of (seed, key)."""
+    with np.errstate(over="ignore"):
+        z = np.uint64(seed & 0xFFFFFFFFFFFFFFFF) + _GAMMA * np.uint64(key + 1)
+    return int(_mix64(np.array([z], dtype=np.uint64))[0])
+
+
+def stream_seed(config: int, channel: int = 0) -> int:
+    return substream(substream(BASE_SEED, config), channel)
+
+
+class RefRng:
+    """The reference Rng (simkit.cpp:19-48) with a numpy-Generator-like surface, vectorised.
+
+    ``random`` / ``uniform`` consume next_uniform() calls and ``standard_normal`` next_gauss()
+    calls in order, exactly as a loop over the reference's methods would (tests/test_workloads.py
+    checks this against the scalar restatement simkit.Rng); the other draws are defined on top:
+    exponential = -scale ln(U), lognormal = exp(mu + sigma Z), integers = lo + floor(U (hi - lo)),
+    permutation = stable argsort of m uniforms."""
+
+    def __init__(self, seed: int):
+        self.state = np.uint64(seed & 0xFFFFFFFFFFFFFFFF)
+        self.spare = None
+
+    def _u64(self, n: int) -> np.ndarray:
+        with np.errstate(over="ignore"):
+            z = self.state + _GAMMA * np.arange(1, n + 1, dtype=np.uint64)
+            self.state = self.state + _GAMMA * np.uint64(n)
+        return _mix64(z)
+
+    def random(self, n=None):
+        m = 1 if n is None else int(n)
+        out = (self._u64(m) >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+        while True:  # next_uniform rejects 0 (probability 2^-53 per draw): refill in order
+            bad = np.flatnonzero(out == 0.0)
+            if bad.size == 0:
+                break
+            i = int(bad[0])
+            out[i:] = np.concatenate([out[i + 1:], (self._u64(1) >> np.uint64(11)).astype(np.float64) * 2.0 ** -53])
+        return float(out[0]) if n is None else out
+
+    def uniform(self, lo=0.0, hi=1.0, n=None):
+        return lo + (hi - lo) * self.random(n)
+
+    def standard_normal(self, n=None):
+        m = 1 if n is None else int(n)
+        out = np.empty(m)
+        k = 0
+        if self.spare is not None and m > 0:
+            out[0] = self.spare
+            self.spare = None
+            k = 1
+        while k < m:
+            need = m - k
+            pairs = max(16, int((need + 1) // 2 * 1.3) + 8)
+            r = self.random(2 * pairs)
+            u, v = 2.0 * r[0::2] - 1.0, 2.0 * r[1::2] - 1.0
+            s = u * u + v * v
+            ok = np.flatnonzero((s < 1.0) & (s != 0.0))
+            if ok.size == 0:
+                continue
+            # a pair is consumed only up to the one that completes the request: rewind the rest
+            used_pairs = int(ok[min(ok.size, (need + 1) // 2) - 1]) + 1
+            acc = ok[ok < used_pairs]
+            f = np.sqrt(-2.0 * np.log(s[acc]) / s[acc])
+            z = np.empty(2 * acc.size)
+            z[0::2] = u[acc] * f
+            z[1::2] = v[acc] * f
+            with np.errstate(over="ignore"):
+                self.state = self.state - _GAMMA * np.uint64(2 * (pairs - used_pairs))
+            take = min(need, z.size)
+            out[k:k + take] = z[:take]
+            k += take
+            if take < z.size:
+                self.spare = float(z[take])
+        return float(out[0]) if n is None else out
+
+    def exponential(self, scale=1.0, n=None):
+        return -scale * np.log(self.random(n))
+
+    def lognormal(self, mu=0.0, sigma=1.0, n=None):
+        return np.exp(mu + sigma * self.standard_normal(n))
+
+    def integers(self, lo, hi, n=None):
+        v = lo + np.floor(self.random(n) * (hi - lo)).astype(np.int64)
+        return int(v) if n is None else v
+
+    def permutation(self, m: int) -> np.ndarray:
+        return np.argsort(self.random(m), kind="stable")
 
 
 @dataclass
@@ -64,7 +167,7 @@ def _strict(t: np.ndarray) -> np.ndarray:
 
 def c1(scale: int = 1) -> Workload:
     """N=4096 from a 256 Hz grid, +-0.3/fs jitter, 20% dropped; 3 lines + AR(2)."""
-    rng = np.random.default_rng(BASE_SEED + 1)
+    rng = RefRng(stream_seed(1))
     fs = 256.0
     n = 4096 // scale
     m = (n * 5) // 4
@@ -85,7 +188,7 @@ def c1(scale: int = 1) -> Workload:
 
 def c2(n: int = 1 << 20, precision: str = "f64", seed_offset: int = 0) -> Workload:
     """Poisson times (mean 1 ms), AR(4) poles 0.95 e^{+-i0.1pi}, e^{+-i0.3pi} + 60 Hz line."""
-    rng = np.random.default_rng(BASE_SEED + 2 + 1000 * seed_offset)
+    rng = RefRng(stream_seed(2, seed_offset))
     while True:
         t = np.cumsum(rng.exponential(1e-3, n))
         t -= t[0]
@@ -108,7 +211,7 @@ def c3(channels: int = 256, n: int = 1 << 18, first_channel: int = 0) -> Workloa
     times = np.empty((channels, n))
     vals = np.empty((channels, n))
     for c in range(channels):
-        rng = np.random.default_rng(BASE_SEED + 3 + 7919 * (first_channel + c))
+        rng = RefRng(stream_seed(3, first_channel + c))
         t = np.arange(n) / fs + rng.uniform(-0.1, 0.1, n) / fs
         for _ in range(int(rng.integers(1, 6))):
             at = int(rng.integers(1, n))
@@ -139,7 +242,7 @@ def c3(channels: int = 256, n: int = 1 << 18, first_channel: int = 0) -> Workloa
 
 def c4(n: int = 1 << 26, n_centers: int = 1 << 24, windows: int = 400) -> Workload:
     """Clustered: 400 nightly windows (lognormal length), Poisson inside; 5 lines + noise."""
-    rng = np.random.default_rng(BASE_SEED + 4)
+    rng = RefRng(stream_seed(4))
     start = np.arange(windows) + rng.uniform(0.0, 0.25, windows)
     length = np.minimum(rng.lognormal(np.log(0.2), 0.5, windows), 0.7)
     share = length / length.sum() * n
@@ -170,7 +273,7 @@ def c4(n: int = 1 << 26, n_centers: int = 1 << 24, windows: int = 400) -> Worklo
 
 def c5(n: int = 1 << 22, k: int = 7, eps: float = 1e-9, precision: str = "f64") -> Workload:
     """Jittered unit grid (+-0.4), 10% dropped; unit white noise."""
-    rng = np.random.default_rng(BASE_SEED + 5)
+    rng = RefRng(stream_seed(5))
     m = int(np.ceil(n / 0.9))
     base = np.arange(m) + rng.uniform(-0.4, 0.4, m)
     keep = np.sort(rng.permutation(m)[:n])
@@ -186,7 +289,7 @@ def c5(n: int = 1 << 22, k: int = 7, eps: float = 1e-9, precision: str = "f64") 
 def small(n: int = 2048, n_centers: Optional[int] = None, k: int = 5, nw: float = 3.0,
           eps: float = 1e-9, seed: int = 0, precision: str = "f64", f_max: float = 0.5) -> Workload:
     """Small jittered/dropout grid for quick parity cases."""
-    rng = np.random.default_rng(BASE_SEED + 100 + seed)
+    rng = RefRng(stream_seed(100, seed))
     m = int(n * 1.25)
     base = np.arange(m) + rng.uniform(-0.35, 0.35, m)
     keep = np.sort(rng.permutation(m)[:n])
