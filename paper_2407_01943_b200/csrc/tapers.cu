@@ -296,6 +296,163 @@ __global__ void __launch_bounds__(32) inverse_iteration_dd_warp_kernel(
   }
 }
 
+
+// ---- DPSS vectors by the eigenvector recurrence, in parallel (large n) ---------------------
+// With sigma within ~1e-11 of the eigenvalue, (T - sigma) x = 0 row by row is the three-term
+// recurrence x_{i+1} = alpha_i x_i + beta_i x_{i-1}, alpha_i = -(d_i - sigma)/e_i,
+// beta_i = -e_{i-1}/e_i.  Run from each end toward the middle, the DPSS grow (edge -> centre) or
+// oscillate (centre), so both recurrences are stable there; they are run from x_0 = 1 (left, rows
+// 0 .. n/2 + w) and from x_{n-1} = 1 (right, the mirrored recurrence, rows n-1 .. n/2 - w - 1) and
+// matched by least squares on the overlap [n/2 - w, n/2 + w] (w = n/64: an odd taper vanishes at
+// the centre, so no single row can be the match).  The recurrence is a product of 2x2 matrices,
+// evaluated in double-double as a three-phase scan: chunk matrices (two basis solutions per
+// chunk of kRecChunk rows, all chunks of all tapers and both halves in parallel), a sequential
+// pass over the chunk matrices for the state at every chunk start, and a parallel re-run of the
+// chunks writing the vector.  This replaces the full-length sequential inverse iteration (one
+// warp per taper over n rows: ~40 s at n = 2^26) of the coarse-start path.
+constexpr int kRecChunk = 2048;
+
+struct RecArgs {
+  const double* d;
+  const double* e;
+  int64_t n, len, nch;  // rows per half (recurrence positions 0 .. len-1), chunks per half
+  const double* sig_hi;
+  const double* sig_lo;
+};
+
+// coefficients of recurrence step i (position i -> i+1) of half h (1: mirrored rows)
+__device__ inline void rec_coef(const RecArgs& A, int h, int64_t i, dd sig, dd& alpha, dd& beta) {
+  const int64_t row = h ? A.n - 1 - i : i;
+  const double ei = h ? A.e[A.n - 2 - i] : A.e[i];        // couples positions i, i+1
+  const double eim1 = h ? A.e[A.n - 1 - i] : A.e[i - 1];  // couples positions i-1, i
+  const dd inv = dd_recip(dd_from(ei));
+  alpha = dd_neg(dd_mul(dd_sub(dd_from(A.d[row]), sig), inv));
+  beta = dd_neg(dd_mul_d(inv, eim1));
+}
+
+// steps of chunk c: i in [1 + c CH, min(1 + (c + 1) CH, len - 1))
+__global__ void rec_chunk_matrix_kernel(const RecArgs A, int k, dd* __restrict__ mats) {
+  const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (g >= static_cast<int64_t>(k) * 2 * A.nch) return;
+  const int64_t c = g % A.nch;
+  const int h = static_cast<int>((g / A.nch) & 1);
+  const int j = static_cast<int>(g / (2 * A.nch));
+  const dd sig = {A.sig_hi[j], A.sig_lo[j]};
+  dd uc = dd_from(1.0), up = dd_from(0.0), vc = dd_from(0.0), vp = dd_from(1.0);
+  const int64_t i0 = 1 + c * kRecChunk, i1 = imin64(1 + (c + 1) * kRecChunk, A.len - 1);
+  for (int64_t i = i0; i < i1; ++i) {
+    dd al, be;
+    rec_coef(A, h, i, sig, al, be);
+    const dd un = dd_add(dd_mul(al, uc), dd_mul(be, up));
+    const dd vn = dd_add(dd_mul(al, vc), dd_mul(be, vp));
+    up = uc;
+    uc = un;
+    vp = vc;
+    vc = vn;
+  }
+  dd* m = mats + 4 * g;  // end = [uc vc; up vp] (cur, prev) of the chunk's start state
+  m[0] = uc;
+  m[1] = vc;
+  m[2] = up;
+  m[3] = vp;
+}
+
+__global__ void rec_prefix_kernel(const RecArgs A, int k, const dd* __restrict__ mats, dd* __restrict__ starts) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= 2 * k) return;
+  const int h = g & 1, j = g >> 1;
+  const dd sig = {A.sig_hi[j], A.sig_lo[j]};
+  // x_0 = 1, x_1 = -(d_0 - sigma) / e_0  (mirrored for h = 1)
+  const double e0 = h ? A.e[A.n - 2] : A.e[0];
+  const int64_t row0 = h ? A.n - 1 : 0;
+  dd cur = dd_neg(dd_mul(dd_sub(dd_from(A.d[row0]), sig), dd_recip(dd_from(e0)))), prev = dd_from(1.0);
+  const dd* m = mats + 4 * static_cast<int64_t>(g) * A.nch;
+  dd* st = starts + 2 * static_cast<int64_t>(g) * A.nch;
+  for (int64_t c = 0; c < A.nch; ++c) {
+    st[2 * c] = cur;
+    st[2 * c + 1] = prev;
+    const dd* mc = m + 4 * c;
+    const dd nc = dd_add(dd_mul(mc[0], cur), dd_mul(mc[1], prev));
+    const dd np = dd_add(dd_mul(mc[2], cur), dd_mul(mc[3], prev));
+    cur = nc;
+    prev = np;
+  }
+}
+
+// positions p: left half writes xs[p] for p <= mid + w; right half writes xs[p] for p > mid + w
+// and ov[p - (mid - w)] for mid - w <= p <= mid + w
+__global__ void rec_expand_kernel(const RecArgs A, int k, const dd* __restrict__ starts, int64_t mid, int64_t w,
+                                  dd* __restrict__ xs, dd* __restrict__ ov) {
+  const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (g >= static_cast<int64_t>(k) * 2 * A.nch) return;
+  const int64_t c = g % A.nch;
+  const int h = static_cast<int>((g / A.nch) & 1);
+  const int j = static_cast<int>(g / (2 * A.nch));
+  const dd sig = {A.sig_hi[j], A.sig_lo[j]};
+  dd* x = xs + static_cast<int64_t>(j) * A.n;
+  dd* o = ov + static_cast<int64_t>(j) * (2 * w + 1);
+  auto put = [&](int64_t q, dd v) {  // recurrence position q of half h
+    const int64_t p = h ? A.n - 1 - q : q;
+    if (h == 0) {
+      if (p <= mid + w) x[p] = v;
+    } else {
+      if (p > mid + w) x[p] = v;
+      else if (p >= mid - w) o[p - (mid - w)] = v;
+    }
+  };
+  dd cur = starts[2 * g], prev = starts[2 * g + 1];
+  const int64_t i0 = 1 + c * kRecChunk, i1 = imin64(1 + (c + 1) * kRecChunk, A.len - 1);
+  if (c == 0) {
+    put(0, prev);
+    put(1, cur);
+  }
+  for (int64_t i = i0; i < i1; ++i) {
+    dd al, be;
+    rec_coef(A, h, i, sig, al, be);
+    const dd nx = dd_add(dd_mul(al, cur), dd_mul(be, prev));
+    prev = cur;
+    cur = nx;
+    put(i + 1, cur);
+  }
+}
+
+// per taper: sums over the overlap of x y and y y, and over the whole vector of x x (after the
+// right half is scaled); double-double partial sums per block
+constexpr int kRecRed = 256;
+__global__ void __launch_bounds__(kRecRed) rec_dot_kernel(const dd* __restrict__ a, const dd* __restrict__ b,
+                                                          int64_t len, int64_t stride_a, int64_t stride_b,
+                                                          dd* __restrict__ partial) {
+  const int j = blockIdx.y;
+  const dd* x = a + static_cast<int64_t>(j) * stride_a;
+  const dd* y = b + static_cast<int64_t>(j) * stride_b;
+  dd acc = dd_from(0.0);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(kRecRed) + threadIdx.x; i < len;
+       i += static_cast<int64_t>(gridDim.x) * kRecRed)
+    acc = dd_add(acc, dd_mul(x[i], y[i]));
+  __shared__ double sh[kRecRed], sl[kRecRed];
+  sh[threadIdx.x] = acc.hi;
+  sl[threadIdx.x] = acc.lo;
+  __syncthreads();
+  for (int o = kRecRed / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      const dd r = dd_add(dd{sh[threadIdx.x], sl[threadIdx.x]}, dd{sh[threadIdx.x + o], sl[threadIdx.x + o]});
+      sh[threadIdx.x] = r.hi;
+      sl[threadIdx.x] = r.lo;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[static_cast<int64_t>(j) * gridDim.x + blockIdx.x] = dd{sh[0], sl[0]};
+}
+
+__global__ void dd_scale_range_kernel(dd* __restrict__ xs, const double* __restrict__ scales, int64_t n, int64_t p0,
+                                      int64_t p1, int k) {
+  const int64_t len = p1 - p0;
+  const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (g >= len * k) return;
+  const int64_t j = g / len, p = p0 + (g - j * len);
+  xs[j * n + p] = dd_mul(xs[j * n + p], dd{scales[2 * j], scales[2 * j + 1]});
+}
+
 // x_j <- x_j * scale_j in double-double (normalised start vectors for a refined second run)
 __global__ void dd_scale_kernel(dd* __restrict__ xs, const double* __restrict__ scales, int64_t n, int k) {
   const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -1097,6 +1254,76 @@ void rayleigh_update(const double* d_diag, const double* d_off, int64_t n, int64
   }
 }
 
+
+// DPSS rows xs [k][n] (double-double, unit norm) by the two-sided recurrence at the shifts sig
+// (rec_* kernels above).
+void dpss_recurrence_vectors(const double* d_diag, const double* d_off, int64_t n, int64_t k,
+                             const std::vector<double>& sig_hi, const std::vector<double>& sig_lo, dd* xs,
+                             cudaStream_t s) {
+  const int64_t mid = n / 2, w = std::max<int64_t>(8, n / 64);
+  RecArgs A{};
+  A.d = d_diag;
+  A.e = d_off;
+  A.n = n;
+  A.len = mid + w + 1;
+  A.nch = (A.len - 2 + kRecChunk - 1) / kRecChunk;
+  DeviceBuffer d_sh(k * sizeof(double)), d_sl(k * sizeof(double));
+  NUS_CUDA(cudaMemcpyAsync(d_sh.ptr, sig_hi.data(), k * sizeof(double), cudaMemcpyHostToDevice, s));
+  NUS_CUDA(cudaMemcpyAsync(d_sl.ptr, sig_lo.data(), k * sizeof(double), cudaMemcpyHostToDevice, s));
+  A.sig_hi = d_sh.as<double>();
+  A.sig_lo = d_sl.as<double>();
+  const int64_t chunks = k * 2 * A.nch;
+  DeviceBuffer mats(static_cast<size_t>(chunks) * 4 * sizeof(dd)), starts(static_cast<size_t>(chunks) * 2 * sizeof(dd));
+  DeviceBuffer ov(static_cast<size_t>(k) * (2 * w + 1) * sizeof(dd));
+  rec_chunk_matrix_kernel<<<blocks_for(chunks, 128), 128, 0, s>>>(A, static_cast<int>(k), mats.as<dd>());
+  note_launch();
+  rec_prefix_kernel<<<blocks_for(2 * k, 32), 32, 0, s>>>(A, static_cast<int>(k), mats.as<dd>(), starts.as<dd>());
+  note_launch();
+  rec_expand_kernel<<<blocks_for(chunks, 128), 128, 0, s>>>(A, static_cast<int>(k), starts.as<dd>(), mid, w, xs,
+                                                            ov.as<dd>());
+  note_launch();
+  check_launch("dpss recurrence");
+  constexpr unsigned kBlocks = 256;
+  DeviceBuffer part(static_cast<size_t>(k) * kBlocks * sizeof(dd));
+  std::vector<dd> hp(static_cast<size_t>(k) * kBlocks);
+  auto dot = [&](const dd* a, const dd* b, int64_t len, int64_t sa, int64_t sb) {
+    rec_dot_kernel<<<dim3(kBlocks, static_cast<unsigned>(k)), kRecRed, 0, s>>>(a, b, len, sa, sb, part.as<dd>());
+    note_launch();
+    check_launch("rec_dot_kernel");
+    NUS_CUDA(cudaMemcpyAsync(hp.data(), part.ptr, hp.size() * sizeof(dd), cudaMemcpyDeviceToHost, s));
+    NUS_CUDA(cudaStreamSynchronize(s));
+    std::vector<long double> r(k, 0.0L);
+    for (int64_t j = 0; j < k; ++j)
+      for (unsigned b2 = 0; b2 < kBlocks; ++b2)
+        r[j] += static_cast<long double>(hp[j * kBlocks + b2].hi) + static_cast<long double>(hp[j * kBlocks + b2].lo);
+    return r;
+  };
+  // match the right half to the left on the overlap (least squares), then normalise
+  const std::vector<long double> xy = dot(xs + (mid - w), ov.as<dd>(), 2 * w + 1, n, 2 * w + 1);
+  const std::vector<long double> yy = dot(ov.as<dd>(), ov.as<dd>(), 2 * w + 1, 2 * w + 1, 2 * w + 1);
+  std::vector<double> sc(2 * k);
+  auto to_dd = [](long double v, double* out) {
+    out[0] = static_cast<double>(v);
+    out[1] = static_cast<double>(v - static_cast<long double>(out[0]));
+  };
+  for (int64_t j = 0; j < k; ++j) {
+    require(yy[j] > 0.0L, "dpss: degenerate recurrence overlap");
+    to_dd(xy[j] / yy[j], &sc[2 * j]);
+  }
+  DeviceBuffer d_sc(2 * k * sizeof(double));
+  NUS_CUDA(cudaMemcpyAsync(d_sc.ptr, sc.data(), sc.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+  const int64_t p0 = mid + w + 1;
+  dd_scale_range_kernel<<<blocks_for((n - p0) * k, 256), 256, 0, s>>>(xs, d_sc.as<double>(), n, p0, n,
+                                                                      static_cast<int>(k));
+  note_launch();
+  const std::vector<long double> xx = dot(xs, xs, n, n, n);
+  for (int64_t j = 0; j < k; ++j) to_dd(1.0L / std::sqrt(xx[j]), &sc[2 * j]);
+  NUS_CUDA(cudaMemcpyAsync(d_sc.ptr, sc.data(), sc.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+  dd_scale_kernel<<<blocks_for(n * k, 256), 256, 0, s>>>(xs, d_sc.as<double>(), n, static_cast<int>(k));
+  note_launch();
+  check_launch("dpss recurrence normalise");
+  NUS_CUDA(cudaStreamSynchronize(s));
+}
 }  // namespace
 
 // DPSS for large n (>= NUS_DPSS_COARSE, default 2^20) without bisection at full length: the DPSS
@@ -1121,7 +1348,7 @@ DpssResult dpss_from_coarse(const double* d_diag, const double* d_off, int64_t n
   DeviceBuffer cv(static_cast<size_t>(k) * nc * sizeof(double));
   dpss_device(nc, tw, k, cv.as<double>(), s);
   lap("coarse dpss");
-  DeviceBuffer xs(static_cast<size_t>(k) * n * sizeof(dd)), us(static_cast<size_t>(k) * n * 3 * sizeof(dd));
+  DeviceBuffer xs(static_cast<size_t>(k) * n * sizeof(dd));
   coarse_start_kernel<<<blocks_for(n * k, 256), 256, 0, s>>>(cv.as<double>(), nc, n, static_cast<int>(k), xs.as<dd>());
   note_launch();
   check_launch("coarse_start_kernel");
@@ -1129,6 +1356,20 @@ DpssResult dpss_from_coarse(const double* d_diag, const double* d_off, int64_t n
   rayleigh_update(d_diag, d_off, n, k, xs.as<dd>(), sig_hi, sig_lo, s);
   rayleigh_update(d_diag, d_off, n, k, xs.as<dd>(), sig_hi, sig_lo, s);
   lap("start vectors + Rayleigh shifts");
+  // default: the parallel two-sided recurrence at the Rayleigh shifts, twice (the second pass at
+  // the shifts of the first pass's vectors); NUS_DPSS_RECURRENCE=0 keeps the sequential inverse
+  // iteration below
+  const char* re = std::getenv("NUS_DPSS_RECURRENCE");
+  const int rec_passes = re ? std::atoi(re) : 2;
+  DeviceBuffer d_norm(2 * k * sizeof(double));
+  if (rec_passes > 0) {
+    for (int pass = 0; pass < rec_passes; ++pass) {
+      dpss_recurrence_vectors(d_diag, d_off, n, k, sig_hi, sig_lo, xs.as<dd>(), s);
+      rayleigh_update(d_diag, d_off, n, k, xs.as<dd>(), sig_hi, sig_lo, s);
+      lap("recurrence + Rayleigh");
+    }
+  } else {
+  DeviceBuffer us(static_cast<size_t>(k) * n * 3 * sizeof(dd));
   // ||T|| for the pivot floor (as tridiag_top_device)
   std::vector<double> hd(n), he(n - 1);
   NUS_CUDA(cudaMemcpyAsync(hd.data(), d_diag, n * sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -1138,7 +1379,7 @@ DpssResult dpss_from_coarse(const double* d_diag, const double* d_off, int64_t n
   for (int64_t i = 0; i < n; ++i)
     anorm = std::max(anorm, std::fabs(hd[i]) + (i > 0 ? std::fabs(he[i - 1]) : 0.0) + (i + 1 < n ? std::fabs(he[i]) : 0.0));
   const double pivmin = std::max(anorm, DBL_MIN) * DBL_EPSILON * 1e-3;
-  DeviceBuffer d_sh(k * sizeof(double)), d_sl(k * sizeof(double)), d_norm(2 * k * sizeof(double));
+  DeviceBuffer d_sh(k * sizeof(double)), d_sl(k * sizeof(double));
   const char* pe = std::getenv("NUS_DPSS_COARSE_ITERS");
   const int passes = pe ? std::max(1, std::atoi(pe)) : 1;  // 1: 1.8e-16 from the bisection path at 2^23 (0: 5e-3)
   for (int pass = 0; pass < passes; ++pass) {
@@ -1153,6 +1394,7 @@ DpssResult dpss_from_coarse(const double* d_diag, const double* d_off, int64_t n
     note_launch();
     rayleigh_update(d_diag, d_off, n, k, xs.as<dd>(), sig_hi, sig_lo, s);
     lap("inverse iteration + Rayleigh");
+  }
   }
   // xs is normalised (scale 1): finalize with unit scales, then the canonical sign
   std::vector<double> ones(2 * k);

@@ -178,8 +178,9 @@ def test_c5_2e22_eps_k_precision_lattice_vs_reference(kern):
 
 @pytest.mark.parametrize("lg", [23, 24])
 def test_dpss_coarse_start_2e23_2e24_vs_long_double(lg):
-    """The default large-N DPSS (coarse start, no full-length bisection) at 2^23 and 2^24, NW 8,
-    K 15 (C4's band), against the long-double bisection + inverse iteration restatement."""
+    """The default large-N DPSS (coarse start + the parallel two-sided recurrence, no full-length
+    bisection or solve) at 2^23 and 2^24, NW 8, K 15 (C4's band), against the long-double bisection
+    + inverse iteration restatement."""
     n = 1 << lg
     d = nus.dpss_uniform(n, 8.0, 15, concentrations=False)
     tc, ev = C.dpss(n, 8.0, 15, threads=THREADS)

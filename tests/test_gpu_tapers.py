@@ -177,3 +177,19 @@ def test_dpss_from_coarse_start_vs_extended_precision_oracle(n, tw, k, monkeypat
     tc, ev = C.dpss(n, tw, k)
     assert np.abs(sign_align(d.tapers, tc) - tc).max() < 1e-10
     np.testing.assert_allclose(d.eigenvalues, ev, rtol=1e-13)
+
+
+@pytest.mark.parametrize("n,tw,k", [(1 << 20, 8.0, 15), (1 << 21, 4.0, 7), (1 << 22, 8.0, 15)])
+def test_dpss_recurrence_vs_inverse_iteration(n, tw, k, monkeypatch):
+    """The large-n vectors (coarse start, default from 2^20) by the parallel two-sided eigenvector
+    recurrence (tapers.cu rec_* kernels, the default) against the sequential double-double inverse
+    iteration they replace (NUS_DPSS_RECURRENCE=0), and both against the long-double restatement."""
+    d_rec = nus.dpss_uniform(n, tw, k, concentrations=False)
+    monkeypatch.setenv("NUS_DPSS_RECURRENCE", "0")
+    d_ii = nus.dpss_uniform(n, tw, k, concentrations=False)
+    monkeypatch.delenv("NUS_DPSS_RECURRENCE")
+    assert np.abs(sign_align(d_rec.tapers, d_ii.tapers) - d_ii.tapers).max() < 1e-14
+    np.testing.assert_allclose(d_rec.eigenvalues, d_ii.eigenvalues, rtol=1e-15)
+    tc, ev = C.dpss(n, tw, k)
+    assert np.abs(sign_align(d_rec.tapers, tc) - tc).max() < 1e-10
+    np.testing.assert_allclose(d_rec.eigenvalues, ev, rtol=1e-13)
