@@ -56,8 +56,9 @@ def make_workload(name, rank):
         return W.c2(precision="f64", seed_offset=rank)
     if name == "c2f32":
         return W.c2(precision="f32", seed_offset=rank)
-    if name == "c3":
-        return W.c3(channels=int(os.environ.get("NUS_C3_CHANNELS", "32")), first_channel=32 * rank)
+    if name == "c3":  # BASELINE C3: 256 channels per replica (NUS_C3_CHANNELS overrides)
+        ch = int(os.environ.get("NUS_C3_CHANNELS", "256"))
+        return W.c3(channels=ch, first_channel=ch * rank)
     if name == "c5":
         return W.c5(k=int(os.environ.get("NUS_C5_K", "7")))
     if name == "c4":  # C4's structure; N defaults to 2^22 (DPSS setup at 2^26)
@@ -173,6 +174,34 @@ def cpu_reference_leg(wl, tapers, threads, spectra_steps, taper_per_step=False):
     return per_step_units / (sum(times) / len(times)), times, per_step_units
 
 
+def cpu_reference_channels(wl, tapers, threads, steps, warmup=1):
+    """The reference CPU path on independent channels (channels in parallel, as the
+    reference's parallel_for): one Injected handle (NufftPlan + eigencoefficients + power loop,
+    oracle/_ref) per channel for `threads` channels, each step = those channels' full K-taper spectra
+    on `threads` host threads.  Returns (points*tapers/s, seconds per step)."""
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle import Injected
+    cnt = min(threads, wl.times.shape[0])
+    hs = [Injected(wl.times[c], tapers[c], wl.centers, wl.eps, wl.f_max, float(wl.f_w[c]), policy=0)
+          for c in range(cnt)]
+    try:
+        with ThreadPoolExecutor(cnt) as ex:
+            def one():
+                list(ex.map(lambda c: hs[c].power(wl.values[c]), range(cnt)))
+            for _ in range(warmup):
+                one()
+            times = []
+            for _ in range(steps):
+                t0 = time.perf_counter()
+                one()
+                times.append(time.perf_counter() - t0)
+    finally:
+        for h in hs:
+            h.close()
+    units = cnt * wl.times.shape[1] * tapers.shape[1]
+    return units / (sum(times) / len(times)), times, cnt
+
+
 def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -187,6 +216,34 @@ def run_reference_arm(args):
         print(json.dumps({"impl": "reference", "unavailable": f"oracle import failed: {e}"}))
         return 0
     threads = max(1, min(os.cpu_count() or 1, 32))
+    if wl.times.ndim == 2:  # independent channels (C3): channels in parallel on the host threads
+        from oracle import C as OC
+        cnt = min(threads, wl.times.shape[0])
+        taps = []
+        for c in range(cnt):  # interpolated DPSS per channel from the restatement, R(B)-normalised
+            t = wl.times[c]
+            n = t.size
+            h = (t[-1] - t[0]) / (n - 1)
+            dp, _ = OC.dpss(n, float(wl.f_w[c]) * h * n, wl.k, threads=threads)
+            knots = t[0] + h * np.arange(n)
+            w = np.stack([OC.spline(knots, dp[j], t) for j in range(wl.k)])
+            taps.append(w)
+        value, ts, cnt = cpu_reference_channels(wl, np.stack(taps), threads, args.steps, args.warmup)
+        line = {
+            "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(ts) / len(ts),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "config": bench_config(wl, args.workload),
+            "parallelism": f"{cnt} channels on {cnt} host threads (rank 0 only)",
+            "window": "Gaussian (the reference's own gridding kernel)",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cnt, "kind": "reference",
+                             "sample": f"per step: {cnt} channels x one full {wl.k}-taper spectrum each "
+                                       f"(N={wl.times.shape[1]}, I={wl.centers.size}) through the reference "
+                                       "NufftPlan + eigencoefficients + power loop, tapers injected"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line), flush=True)
+        return 0
     tapers = reference_tapers(wl)
     from oracle import Injected
     t = wl.times if wl.times.ndim == 1 else wl.times[0]
@@ -547,6 +604,18 @@ def main():
     if rank == 0:
         line["clocks"] = clk.summary()
     # ---- cpu baseline (rank 0, N=1 only)
+    if rank == 0 and world == 1 and not args.no_cpu and wl.times.ndim == 2:
+        try:  # independent channels: the reference on `threads` channels in parallel
+            threads = max(1, min(os.cpu_count() or 1, 32))
+            v, ts, cnt = cpu_reference_channels(wl, est.tapers(), threads, 1)
+            line["cpu_baseline"] = {
+                "value": v, "unit": UNIT, "cores": cnt, "kind": "reference",
+                "sample": f"{cnt} channels x one full {k}-taper spectrum each (N={n}, I={nc}) on {cnt} host "
+                          "threads through the reference's NufftPlan + eigencoefficients + power loop "
+                          "(oracle/_ref), the GPU's tapers injected, 1 timed batch after 1 warm-up",
+                "seconds": ts}
+        except Exception as e:  # pragma: no cover
+            line["cpu_baseline"] = {"value": None, "error": str(e)}
     if rank == 0 and world == 1 and not args.no_cpu and wl.times.ndim == 1:
         try:
             threads = max(1, min(os.cpu_count() or 1, 32))
