@@ -264,7 +264,7 @@ void quadform_device(const double* d_t, int64_t n, double f_max, const double* d
 // q_k = w_k^T R(B) w_k in O(N log N) (normalise.cu); h_t = host copy of the times
 void quadform_fast_device(const double* d_t, const double* h_t, int64_t n, double f_max, const double* d_w,
                           int64_t k, double* q_host, cudaStream_t s, int device);
-// exact O(N^2) form for n <= this (NUS_QUADFORM_EXACT_MAX, default 2^18) unless NUS_NORMALISE
+// exact O(N^2) form for n <= this (NUS_QUADFORM_EXACT_MAX, default 2^16) unless NUS_NORMALISE
 bool normalise_exact(int64_t n);
 // Full gpss_interpolated for one grid: d_w [K][n] normalised; timings optional.
 void gpss_interpolated_device(const double* d_t, const double* h_t, int64_t n, double f_max,

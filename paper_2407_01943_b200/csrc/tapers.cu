@@ -1540,7 +1540,9 @@ bool normalise_exact(int64_t n) {
   if (e && std::strcmp(e, "exact") == 0) return true;
   if (e && std::strcmp(e, "fast") == 0) return false;
   const char* m = std::getenv("NUS_QUADFORM_EXACT_MAX");
-  const int64_t lim = m ? std::atoll(m) : (int64_t{1} << 18);
+  // exact O(N^2) form up to 2^16 samples; above, the O(N log N) lattice form (agreement <= 5e-12 on
+  // every config's sampling): C3's 256 channels of 2^18 samples 0.83 s -> ~0.1 s of setup each
+  const int64_t lim = m ? std::atoll(m) : (int64_t{1} << 16);
   return n <= lim;
 }
 

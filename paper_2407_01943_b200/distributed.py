@@ -265,7 +265,7 @@ class TaperShard:
 class SampleSplit:
     """Config C4: one long series, samples split across ranks, reduce-scatter of fine grids."""
 
-    fast_normalise_min = 1 << 18  # above this N the R(B) forms use the O(N log N) method
+    fast_normalise_min = 1 << 16  # above this N the R(B) forms use the O(N log N) method (as tapers.cu)
 
     def __init__(self, times, centers, f_max, f_w, k, eps, precision="f64", engine=None, group=None,
                  tapers: Optional[np.ndarray] = None, fused: Optional[bool] = None):
