@@ -98,11 +98,12 @@ std::unique_ptr<Estimator> estimator_create(const nus_mtnufft_config_t& cfg, con
   } else {
     require(cfg.f_max > 0.0 && std::isfinite(cfg.f_max), "SignalBand: f_max must be positive");
     DeviceBuffer dt(n * sizeof(double));
+    DpssCache dpss_cache;  // channels whose f_w h N is the same double share one DPSS
     for (int64_t c = 0; c < C; ++c) {
       NUS_CUDA(cudaMemcpy(dt.ptr, times + c * n, n * sizeof(double), cudaMemcpyHostToDevice));
       double a = 0, b = 0, d = 0;
       gpss_interpolated_device(dt.as<double>(), times + c * n, n, cfg.f_max, est->f_w[c], K,
-                               est->tapers_time.as<double>() + c * K * n, s, &a, &b, &d);
+                               est->tapers_time.as<double>() + c * K * n, s, &a, &b, &d, &dpss_cache);
       est->setup_ms[0] += a;
       est->setup_ms[1] += b;
       est->setup_ms[2] += d;

@@ -266,11 +266,23 @@ void quadform_fast_device(const double* d_t, const double* h_t, int64_t n, doubl
                           int64_t k, double* q_host, cudaStream_t s, int device);
 // exact O(N^2) form for n <= this (NUS_QUADFORM_EXACT_MAX, default 2^16) unless NUS_NORMALISE
 bool normalise_exact(int64_t n);
+// Uniform-grid DPSS kept across the channels of one estimator: the vectors depend only on
+// (n, time-bandwidth product, k), and channels of one recording share them whenever f_w h N
+// rounds to the same double (C3: 256 channels, 2-3 distinct values).  Exact-key match only.
+struct DpssCache {
+  struct Entry {
+    int64_t n = 0, k = 0;
+    double tw = 0.0;
+    DeviceBuffer dp;  // [k][n]
+  };
+  std::vector<Entry> entries;
+  int64_t hits = 0;
+};
 // Full gpss_interpolated for one grid: d_w [K][n] normalised; timings optional.
 void gpss_interpolated_device(const double* d_t, const double* h_t, int64_t n, double f_max,
                               double f_w, int64_t k, double* d_w, cudaStream_t s,
                               double* ms_dpss = nullptr, double* ms_spline = nullptr,
-                              double* ms_norm = nullptr);
+                              double* ms_norm = nullptr, DpssCache* cache = nullptr);
 
 __host__ __device__ inline int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }
 __host__ __device__ inline int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }

@@ -633,15 +633,15 @@ struct StPoint {  // this lane's prefetched point: raw loads only
 };
 
 // Loads of batch [b0, b0 + nb) of unit u (nb >= 1): every load unconditional (clamped index), so
-// no merge waits on HBM; lanes past the batch get ti = -1 (x masked to 0 at staging).
+// no merge waits on HBM; lanes past the batch get ti = -1 (x masked to 0 at staging).  `base` is the
+// channel's first point (u.c * n) and `tp0` its first taper row at point 0, both fixed per unit.
 template <typename Real, int XK, int KG, int NS>
-__device__ inline void st_load(StPoint<Real, KG>& q, int ti, const StUnit& u, int b0, int nb, int lane,
-                               const SpreadParams<Real>& P) {
+__device__ inline void st_load(StPoint<Real, KG>& q, int ti, const StUnit& u, int64_t base, const Real* tp0, int b0,
+                               int nb, int lane, const SpreadParams<Real>& P) {
   using R2 = typename Vec2<Real>::T;
   const bool has = lane < nb;
   const int qq = b0 + (has ? lane : nb - 1);
   const int pi = st_point(u, qq);
-  const int64_t base = static_cast<int64_t>(u.c) * P.n;
   const int64_t gi = base + pi;
   q.q = qq;
   q.ti = has ? ti : -1;
@@ -664,9 +664,13 @@ __device__ inline void st_load(StPoint<Real, KG>& q, int ti, const StUnit& u, in
     q.fr = ag.x;
     q.fg = ag.y;
   }
-  const Real* tp = P.taper_base + (static_cast<int64_t>(u.c) * P.k_total + P.k0) * P.tstride_k + pi * P.tstride_j;
+  // rows k >= kg re-read row kg - 1 (never staged): the pointer stops advancing there
+  const Real* tp = tp0 + static_cast<int64_t>(pi) * P.tstride_j;
 #pragma unroll
-  for (int k = 0; k < KG; ++k) q.w[k] = tp[min(k, P.kg - 1) * P.tstride_k];
+  for (int k = 0; k < KG; ++k) {
+    q.w[k] = *tp;
+    tp += (k + 1 < P.kg) ? P.tstride_k : 0;
+  }
 }
 
 // perm index of this lane's point of batch b0 (clamped into the stream)
@@ -676,84 +680,105 @@ __device__ inline int st_perm(const StUnit& u, int b0, int lane, const SpreadPar
   return P.perm[static_cast<int64_t>(u.c) * P.n + (u.len > 0 ? st_point(u, q) : 0)];
 }
 
-// Store window blocks PH .. PH + 3 of the accumulator ring (cells `cell` .. + 31 of channel c)
-// and clear them for reuse as the window's upper half.
-template <int PH, typename Real>
-__device__ __forceinline__ void st_flush(double (&cr)[8][2], double (&ci)[8][2], int c, int cell, int g, int t,
-                                         const SpreadParams<Real>& P) {
+// Where a lane's two tapers (2t, 2t + 1 of the launch's group) of channel c go: fixed per unit.
+template <typename Real>
+struct StOut {
+  typename Vec2<Real>::T *p0, *p1;
+  bool ok0, ok1;
+};
+template <typename Real>
+__device__ inline StOut<Real> st_out(int c, int t, const SpreadParams<Real>& P) {
   using R2 = typename Vec2<Real>::T;
-  const bool k0ok = 2 * t < P.kg, k1ok = 2 * t + 1 < P.kg;
-  R2* out0;
-  R2* out1;
+  StOut<Real> o;
+  o.ok0 = 2 * t < P.kg;
+  o.ok1 = 2 * t + 1 < P.kg;
   if (P.slots) {  // taper k -> owner k / per, its slot row k % per (possibly a peer GPU)
-    const int64_t ka = P.k0 + (k0ok ? 2 * t : 0), kb = P.k0 + (k1ok ? 2 * t + 1 : 0);
-    out0 = P.slots[ka / P.per] + (ka % P.per) * P.mr;
-    out1 = P.slots[kb / P.per] + (kb % P.per) * P.mr;
+    const int64_t ka = P.k0 + (o.ok0 ? 2 * t : 0), kb = P.k0 + (o.ok1 ? 2 * t + 1 : 0);
+    o.p0 = P.slots[ka / P.per] + (ka % P.per) * P.mr;
+    o.p1 = P.slots[kb / P.per] + (kb % P.per) * P.mr;
   } else {
     R2* out = P.grid + (static_cast<int64_t>(c) * P.kpad + P.k0) * P.mr;
-    out0 = out + static_cast<int64_t>(2 * t) * P.mr;
-    out1 = out0 + P.mr;
+    o.p0 = out + static_cast<int64_t>(2 * t) * P.mr;
+    o.p1 = o.p0 + P.mr;
   }
+  return o;
+}
+
+// Store window blocks PH .. PH + 3 of the accumulator ring (cells `cell` .. + 31, cell a multiple
+// of 32) and clear them for reuse as the window's upper half.  In the blocked layout the 32 cells
+// share their row j1, so block b sits at a fixed offset from block 0: d1 for b = 1, d2 for b = 2,
+// d1 + d2 for b = 3 (8 b cells on: ((8b) >> lgCW) tiles + (8b) mod CW; natural layout: 8 b).
+template <int PH, typename Real>
+__device__ __forceinline__ void st_flush(double (&cr)[8][2], double (&ci)[8][2], const StOut<Real>& o, int cell,
+                                         int g, int d1, int d2, const SpreadParams<Real>& P) {
+  using R2 = typename Vec2<Real>::T;
+  const int a0 = cell_addr32(cell + g, P.blocked, P.lgC, P.lgCW, P.lgT);
 #pragma unroll
   for (int b = 0; b < 4; ++b) {
-    const int addr = cell_addr32(cell + g + 8 * b, P.blocked, P.lgC, P.lgCW, P.lgT);
-    if (k0ok) out0[addr] = R2{static_cast<Real>(cr[PH + b][0]), static_cast<Real>(ci[PH + b][0])};
-    if (k1ok) out1[addr] = R2{static_cast<Real>(cr[PH + b][1]), static_cast<Real>(ci[PH + b][1])};
+    const int addr = a0 + ((b & 1) ? d1 : 0) + ((b & 2) ? d2 : 0);
+    if (o.ok0) o.p0[addr] = R2{static_cast<Real>(cr[PH + b][0]), static_cast<Real>(ci[PH + b][0])};
+    if (o.ok1) o.p1[addr] = R2{static_cast<Real>(cr[PH + b][1]), static_cast<Real>(ci[PH + b][1])};
     cr[PH + b][0] = cr[PH + b][1] = ci[PH + b][0] = ci[PH + b][1] = 0.0;
   }
 }
 
-// One accumulation pass over the staged points [pst, pend) for the 8 window blocks (block b in
-// registers cr[b], ci[b]).  Per block its point range [lo, hi) comes from two ballots (rel ascends
-// over the lanes), then exact 4-point steps on the tensor cores.  ES (NS > 0): the W rows are zero
-// off the point's support and an ns <= 16 support cannot alias a block cell mod 32 for a point of
-// [lo, hi), so a = W[point][cell mod 32] as stored, masked only past hi; the Gaussian (NS = 0, up
-// to 32 cells, rows not cleared) also masks cells outside the point's support.
-template <int NS, int RS, int PTS>
-__device__ __forceinline__ void st_pass(double (&cr)[8][2], double (&ci)[8][2], int rel, int wb, int w2, int pst,
-                                        int pend, const double* sw, const double2* sz, const int* srel, int g,
-                                        int t) {
+// One accumulation pass over the staged points [pst, pend) for the 8 window blocks.  The window is
+// a RING over the accumulator registers: register block r holds window block (r + 4 ph) & 7, ph the
+// ring phase, so a slide is a store + clear of the old lower half and a phase flip, never a register
+// move -- and because a W row's slot of cell 8 b + g is 8 (r & 3) + g in either phase, both phases
+// run the same code (only the blocks' point ranges are picked by ph).  Per block its point range
+// [lo, hi) comes from byte-packed counts summed over the warp (rel ascends over the lanes:
+// lo = #points whose support ends below the block, hi = #points that start at or below its last
+// cell; one 32-bit warp sum yields four blocks' counts), then exact 4-point steps on the tensor
+// cores.  ES (NS > 0): the W rows are zero off the point's support and an ns <= 16 support cannot
+// alias a block cell mod 32 for a point of [lo, hi), so a = W[point][cell mod 32] as stored, masked
+// only past hi; the Gaussian (NS = 0, up to 32 cells, rows not cleared) also masks cells outside
+// the point's support.
+template <int NS, int RS>
+__device__ __forceinline__ void st_pass(double (&cr)[8][2], double (&ci)[8][2], int rel, int wb, int ph, int w2,
+                                        int pst, int pend, const double* sw, const double2* sz, const int* srel,
+                                        int g, int t) {
   const double* wrow = sw + g;            // + point row * RS + slot base
   const double2* zcol = sz + g * RS + t;  // + p0
   const int* rcol = srel + t;
+  // first block at or past this lane's point start / first block past its support, clamped to 0..8
+  const int d = rel - wb;
+  const int sf = min(max(d >> 3, 0), 8);
+  const int sl = min(max(((d + w2 - 1) >> 3) + 1, 0), 8);
+  const unsigned long long ones = 0x0101010101010101ull;
+  const unsigned long long vf = sf < 8 ? ones << (8 * sf) : 0ull, vl = sl < 8 ? ones << (8 * sl) : 0ull;
+  const unsigned hi03 = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(vf));
+  const unsigned hi47 = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(vf >> 32));
+  const unsigned lo03 = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(vl));
+  const unsigned lo47 = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(vl >> 32));
+  // counts of register blocks 0..3 (A) and 4..7 (B): window blocks 0..3 / 4..7, swapped in phase 1
+  const unsigned hiA = ph ? hi47 : hi03, hiB = ph ? hi03 : hi47;
+  const unsigned loA = ph ? lo47 : lo03, loB = ph ? lo03 : lo47;
+  const int wbA = wb + (ph ? 32 : 0), wbB = wb + (ph ? 0 : 32);
 #pragma unroll
-  for (int b = 0; b < 8; ++b) {
-    const int cb = wb + 8 * b;  // block's first cell
-    const int lo = max(pst, __popc(__ballot_sync(0xffffffffu, rel < cb - (w2 - 1))));
-    const int hi = min(pend, __popc(__ballot_sync(0xffffffffu, rel < cb + 8)));
+  for (int r = 0; r < 8; ++r) {
+    const int cb = (r < 4 ? wbA : wbB) + 8 * (r & 3);  // block's first cell
+    const int lo = max(pst, static_cast<int>(((r < 4 ? loA : loB) >> (8 * (r & 3))) & 0xffu));
+    const int hi = min(pend, static_cast<int>(((r < 4 ? hiA : hiB) >> (8 * (r & 3))) & 0xffu));
     for (int p0 = lo; p0 < hi; p0 += 4) {
-      const int pi = p0 + t;  // rows up to hi + 3 <= 34 < PTS: the overrun rows are zero
-      double a = wrow[pi * RS + ((8 * b) & 31)];
+      const int pi = p0 + t;  // rows up to hi + 3 <= 34 < 35: the overrun rows are zero
+      double a = wrow[pi * RS + 8 * (r & 3)];
       bool keep = pi < hi;
       if constexpr (NS == 0) keep = keep && static_cast<unsigned>(cb + g - rcol[p0]) < static_cast<unsigned>(w2);
       a = keep ? a : 0.0;
       const double2 zb = zcol[p0];
-      dmma_8x8x4(cr[b][0], cr[b][1], a, zb.x);
-      dmma_8x8x4(ci[b][0], ci[b][1], a, zb.y);
+      dmma_8x8x4(cr[r][0], cr[r][1], a, zb.x);
+      dmma_8x8x4(ci[r][0], ci[r][1], a, zb.y);
     }
-  }
-  (void)PTS;
-}
-
-// Store the window's lower 32 cells (blocks 0..3, cells `cell` .. + 31 of channel c), then slide:
-// the upper half becomes the lower one and the upper half restarts at zero.
-template <typename Real>
-__device__ __forceinline__ void st_flush_slide(double (&cr)[8][2], double (&ci)[8][2], int c, int cell, int g, int t,
-                                               const SpreadParams<Real>& P) {
-  st_flush<0, Real>(cr, ci, c, cell, g, t, P);
-#pragma unroll
-  for (int b = 0; b < 4; ++b) {
-    cr[b][0] = cr[b + 4][0];
-    cr[b][1] = cr[b + 4][1];
-    ci[b][0] = ci[b + 4][0];
-    ci[b][1] = ci[b + 4][1];
-    cr[b + 4][0] = cr[b + 4][1] = ci[b + 4][0] = ci[b + 4][1] = 0.0;
   }
 }
 
 // KG: taper rows loaded per point (8: up to 8 tapers, P.kg of them real; 1: one taper / untapered)
 template <typename Real, int XK, int NS, int KG>
-__global__ void __launch_bounds__(kStWarps * 32, 4) spread_stream_kernel(const SpreadParams<Real> P) {
+#ifndef NUS_ST_CTAS
+#define NUS_ST_CTAS 4
+#endif
+__global__ void __launch_bounds__(kStWarps * 32, NUS_ST_CTAS) spread_stream_kernel(const SpreadParams<Real> P) {
   using R2 = typename Vec2<Real>::T;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int RS = kTcRows;
@@ -780,10 +805,17 @@ __global__ void __launch_bounds__(kStWarps * 32, 4) spread_stream_kernel(const S
   const int gw = static_cast<int>(blockIdx.x) * kStWarps + warp;
   const int unit_end = P.warp_first[gw + 1];
   int erase_rel = 1 << 20;  // ES: support of this lane's previous point, cleared before restaging
+  int ph = 0;               // ring phase of the accumulator window (st_pass)
+  // offsets of window blocks 1 and 2 from block 0 in the grid layout (st_flush)
+  const int d1 = P.blocked ? ((8 >> P.lgCW) << P.lgT) + (8 & ((1 << P.lgCW) - 1)) : 8;
+  const int d2 = P.blocked ? ((16 >> P.lgCW) << P.lgT) + (16 & ((1 << P.lgCW) - 1)) : 16;
   for (int unit = P.warp_first[gw]; unit < unit_end; ++unit) {
     const StUnit u = st_unit(unit, P);
+    const StOut<Real> out = st_out<Real>(u.c, t, P);
+    const int64_t base = static_cast<int64_t>(u.c) * P.n;
+    const Real* tp0 = P.taper_base + (static_cast<int64_t>(u.c) * P.k_total + P.k0) * P.tstride_k;
     int wb = 0;  // window base, cells relative to the unit's first cell
-    if (u.len > 0) st_load<Real, XK, KG, NS>(pt, st_perm(u, 0, lane, P), u, 0, min(32, u.len), lane, P);
+    if (u.len > 0) st_load<Real, XK, KG, NS>(pt, st_perm(u, 0, lane, P), u, base, tp0, 0, min(32, u.len), lane, P);
     int perm_next = st_perm(u, 32, lane, P);
     for (int b0 = 0; b0 < u.len; b0 += 32) {
       // ---- stage batch [b0, b0 + nb): lane = point; z column, rel, and the W row (support only)
@@ -853,7 +885,7 @@ __global__ void __launch_bounds__(kStWarps * 32, 4) spread_stream_kernel(const S
       __syncwarp();
       // ---- prefetch the next batch (its perm is in hand) and the perm of the one after
       if (b0 + 32 < u.len) {
-        st_load<Real, XK, KG, NS>(pt, perm_next, u, b0 + 32, min(32, u.len - b0 - 32), lane, P);
+        st_load<Real, XK, KG, NS>(pt, perm_next, u, base, tp0, b0 + 32, min(32, u.len - b0 - 32), lane, P);
         perm_next = st_perm(u, b0 + 64, lane, P);
       }
       // ---- accumulate the prefix of the batch whose supports fit the window; when the next point's
@@ -863,23 +895,29 @@ __global__ void __launch_bounds__(kStWarps * 32, 4) spread_stream_kernel(const S
       for (;;) {
         const int pend = __popc(__ballot_sync(0xffffffffu, has && rel + (w2 - 1) < wb + 64));
         if (pend > pst) {
-          st_pass<NS, RS, PTS>(cr, ci, rel, wb, w2, pst, pend, sw, sz, srel, g, t);
+          st_pass<NS, RS>(cr, ci, rel, wb, ph, w2, pst, pend, sw, sz, srel, g, t);
           pst = pend;
         }
         if (pst >= nb) break;
-        st_flush_slide<Real>(cr, ci, u.c, u.cell0 + wb, g, t, P);
+        // the lower 32 cells are complete: store and clear them (they become the upper half)
+        if (ph == 0) st_flush<0, Real>(cr, ci, out, u.cell0 + wb, g, d1, d2, P);
+        else st_flush<4, Real>(cr, ci, out, u.cell0 + wb, g, d1, d2, P);
+        ph ^= 1;
         wb += 32;
       }
       __syncwarp();  // private tables are restaged next
     }
     // end of the unit: store the rest of its cells (zeros past the last point)
     while (wb < u.ncell) {
-      st_flush_slide<Real>(cr, ci, u.c, u.cell0 + wb, g, t, P);
+      if (ph == 0) st_flush<0, Real>(cr, ci, out, u.cell0 + wb, g, d1, d2, P);
+      else st_flush<4, Real>(cr, ci, out, u.cell0 + wb, g, d1, d2, P);
+      ph ^= 1;
       wb += 32;
     }
-    // the lower half now holds contributions past the unit's last cell: discard them
+    // what is left holds contributions past the unit's last cell: discard them
 #pragma unroll
-    for (int b = 0; b < 4; ++b) cr[b][0] = cr[b][1] = ci[b][0] = ci[b][1] = 0.0;
+    for (int b = 0; b < 8; ++b) cr[b][0] = cr[b][1] = ci[b][0] = ci[b][1] = 0.0;
+    ph = 0;
   }
   if (P.slots) __threadfence_system();  // peer-slot stores ordered before the caller's barrier
 }

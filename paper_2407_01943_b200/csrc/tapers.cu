@@ -1548,7 +1548,7 @@ bool normalise_exact(int64_t n) {
 
 void gpss_interpolated_device(const double* d_t, const double* h_t, int64_t n, double f_max,
                               double f_w, int64_t k, double* d_w, cudaStream_t s, double* ms_dpss,
-                              double* ms_spline, double* ms_norm) {
+                              double* ms_spline, double* ms_norm, DpssCache* cache) {
   // tapers.cpp:146-160 validation, same order and exception types
   require(n >= 8, "gpss_interpolated: need at least 8 samples");
   require(f_w > 0.0, "gpss_interpolated: f_w must be positive");
@@ -1560,11 +1560,32 @@ void gpss_interpolated_device(const double* d_t, const double* h_t, int64_t n, d
   const double tw = f_w * h * static_cast<double>(n);
   require(tw < static_cast<double>(n) / 2.0, "gpss_interpolated: f_w too large for this grid");
   auto t0 = std::chrono::steady_clock::now();
-  DeviceBuffer dp(static_cast<size_t>(k) * n * sizeof(double));
-  dpss_device(n, tw, k, dp.as<double>(), s);
+  DeviceBuffer own;
+  const double* dpv = nullptr;
+  if (cache) {
+    for (const DpssCache::Entry& e : cache->entries)
+      if (e.n == n && e.k == k && e.tw == tw) {
+        dpv = e.dp.as<double>();
+        ++cache->hits;
+        break;
+      }
+  }
+  if (!dpv) {
+    own.alloc(static_cast<size_t>(k) * n * sizeof(double));
+    dpss_device(n, tw, k, own.as<double>(), s);
+    dpv = own.as<double>();
+    if (cache) {
+      cache->entries.emplace_back();
+      DpssCache::Entry& e = cache->entries.back();
+      e.n = n;
+      e.k = k;
+      e.tw = tw;
+      e.dp = std::move(own);
+    }
+  }
   if (ms_dpss) *ms_dpss = host_ms_since(t0);
   t0 = std::chrono::steady_clock::now();
-  spline_uniform_device(d_t, n, dp.as<double>(), k, d_w, s);
+  spline_uniform_device(d_t, n, dpv, k, d_w, s);
   if (ms_spline) *ms_spline = host_ms_since(t0);
   t0 = std::chrono::steady_clock::now();
   std::vector<double> q(k), scale(k);
