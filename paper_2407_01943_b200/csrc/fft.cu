@@ -118,13 +118,34 @@ __device__ inline void dft_reg(T2* v) {
   dit_stages<R, 2>(v);
 }
 
-// Shared-memory index of logical element e.  Row buffers (pass B) use the XOR swizzle
-// e ^ ((e >> 4) & 7), which makes every Stockham stage bank-conflict free for 16-byte
-// elements (the first stage stores at stride 16); column buffers (pass A) are laid out
-// column-fastest and are conflict-free as is.
-template <bool SWZ>
-__device__ inline int sidx(int e) {
-  return SWZ ? (e ^ ((e >> 4) & 7)) : e;
+// Shared-memory index of logical element e: an XOR swizzle chosen per buffer kind, element size and
+// exchange so that each wavefront's W lanes (8 lanes of 16-byte elements, 16 of 8-byte ones) meet
+// distinct banks in both the stores of one stage and the loads of the next (lanes j' = consecutive
+// elements: any XOR of the low lg W bits by higher bits keeps the loads conflict-free).
+//   Row buffers (pass B, SWZ).  First exchange: the radix-R0 stage 0 stores lane j at R0 j + q, so the
+//   low bits take j's: (e >> lg R0) & (W - 1) when R0 >= W, else (e >> lg W) & (R0 - 1).  Later
+//   exchanges: stage stores of stride >= 16 (and the Ns = R0 < W store, whose lanes j, j + Ns sit
+//   16 Ns apart) are spread by (e >> 4) & (W - 1).
+//   Column buffers (pass A): element (column f, row) at f + CW row, lanes column-fastest; with fewer
+//   columns than lanes per wavefront (CW = 4: Mr = 2^21, 2^22) the wavefront spans n = W / CW rows,
+//   which the radix-R0 stage-0 stores put CW R0 apart: the row's bits [lg R0, lg R0 + lg n) are
+//   XORed into the index bits [lg CW, lg W) (needs R0 >= n, which keeps every later stage's store and
+//   load conflict-free too).
+// `first`: the exchange between stage 0 and stage 1.
+template <bool SWZ, int R0, int ESZ>
+__device__ __forceinline__ int sidx(int e, bool first, int lgNfft) {
+  constexpr int lgW = ESZ == 16 ? 3 : 4;
+  constexpr int W = 1 << lgW;
+  constexpr int lgR0 = R0 == 16 ? 4 : R0 == 8 ? 3 : R0 == 4 ? 2 : 1;
+  if constexpr (SWZ) {
+    const int h0 = R0 >= W ? (e >> lgR0) & (W - 1) : (e >> lgW) & (R0 - 1);
+    const int h1 = (e >> 4) & (W - 1);
+    return e ^ (first ? h0 : h1);
+  } else {
+    const int lgn = lgW - lgNfft;
+    if (lgn <= 0 || lgR0 < lgn) return e;
+    return e ^ (((e >> (lgNfft + lgR0)) & ((1 << lgn) - 1)) << lgNfft);
+  }
 }
 
 // Register-resident FFT: the thread holds 16 elements.  Stage 0 (radix R0 in {2,4,8,16},
@@ -161,7 +182,7 @@ __device__ __forceinline__ void fft16_regs(T2 (&v)[16], T2* buf, int lgL, int lg
       const int f = u & nfm, j = (u >> lgNfft) & ((1 << lgNb) - 1);
       const int base = f * fs + (j << lgR0) * es;  // Ns = 1: out = j*R0 + q
 #pragma unroll
-      for (int q = 0; q < R0; ++q) buf[sidx<SWZ>(base + q * es)] = g[q];
+      for (int q = 0; q < R0; ++q) buf[sidx<SWZ, R0, sizeof(T2)>(base + q * es, true, lgNfft)] = g[q];
     }
   }
   group_bar<NT>(bar);
@@ -179,7 +200,7 @@ __device__ __forceinline__ void fft16_regs(T2 (&v)[16], T2* buf, int lgL, int lg
     T2 wq = w1;
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
-      T2 x = buf[sidx<SWZ>(in0 + (q << lgNb) * es)];
+      T2 x = buf[sidx<SWZ, R0, sizeof(T2)>(in0 + (q << lgNb) * es, lgNs == lgR0, lgNfft)];
       if (q) {
         x = cmul(x, wq);
         wq = cmul(wq, w1);
@@ -191,7 +212,7 @@ __device__ __forceinline__ void fft16_regs(T2 (&v)[16], T2* buf, int lgL, int lg
     if (lgNs + 4 < lgL) {
       group_bar<NT>(bar);
 #pragma unroll
-      for (int q = 0; q < 16; ++q) buf[sidx<SWZ>(outb + (q << lgNs) * es)] = v[q];
+      for (int q = 0; q < 16; ++q) buf[sidx<SWZ, R0, sizeof(T2)>(outb + (q << lgNs) * es, false, lgNfft)] = v[q];
       group_bar<NT>(bar);
     } else {
       f_out = f;

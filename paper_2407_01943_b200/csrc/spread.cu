@@ -1243,6 +1243,10 @@ std::vector<SpreadLaunch> spread_schedule(const Plan& plan, int64_t k, bool x_co
     const char* e = std::getenv("NUS_SPREAD_GROUPS");
     return !(e && std::strcmp(e, "1") == 0);
   }();
+  static const bool two_forced = [] {
+    const char* e = std::getenv("NUS_SPREAD_GROUPS");
+    return e && std::strcmp(e, "2") == 0;
+  }();
   // two groups per staging: C3 (fp32, K = 9, ns = 6) 781 vs 1085 us against two per-segment
   // single-group launches, C4's structure 543 vs 623 us; slower with the narrowest window (ns = 4)
   // unless the data is dense
@@ -1255,7 +1259,12 @@ std::vector<SpreadLaunch> spread_schedule(const Plan& plan, int64_t k, bool x_co
   const bool dense = p.n >= dense_min * nseg_used || p.sw >= 6;
   const SpreadLaunch::Kind single = !tc ? SpreadLaunch::kGather : use_stream ? SpreadLaunch::kStream : SpreadLaunch::kSegment;
   std::vector<SpreadLaunch> out;
-  if (tc && two_ok && dense && k > 8 && !x_complex) {  // launches of <= 16 tapers, balanced
+  // fp32 plans take streaming launches instead (C3, 32 channels x 2^18, K = 9, ns = 6: two streaming
+  // launches 789 us vs 937 us for the two-group kernel, whose 41-point segments need two staging
+  // rounds each); in fp64 the two-group kernel stays ahead on HBM-streamed tables (C4's structure
+  // 4.72 vs 5.98 ms, C5 at K = 15 703 vs 739 us).  NUS_SPREAD_GROUPS=2 forces it, =1 turns it off.
+  const bool two_pref = two_forced || !(use_stream && p.precision == NUS_F32);
+  if (tc && two_ok && two_pref && dense && k > 8 && !x_complex) {  // launches of <= 16 tapers, balanced
     const int64_t launches = (k + 15) / 16;
     int64_t kb = 0;
     for (int64_t li = 0; li < launches; ++li) {
