@@ -400,8 +400,11 @@ __host__ __device__ constexpr int crop_q(int c) { return c < 5 ? c : c + 7; }
 __host__ __device__ constexpr int lg_threads(int nt) { return nt <= 1 ? 0 : 1 + lg_threads(nt / 2); }
 
 // NT = 32 / 64 (C = 512 / 1024): single-pass transforms of small grids (R = 1), several rows per SM.
+#ifndef NUS_ROWS_F32_CTAS
+#define NUS_ROWS_F32_CTAS 7
+#endif
 template <typename Real, typename PReal, int R0, int NT = kFftThreads>
-__global__ void __launch_bounds__(NT, NT <= 64 ? 8 : NT == 128 ? (sizeof(Real) == 4 ? 6 : 4) : NT == 256 ? (sizeof(Real) == 4 ? 3 : 2) : 1) fft_rows_crop_kernel(
+__global__ void __launch_bounds__(NT, NT <= 64 ? 8 : NT == 128 ? (sizeof(Real) == 4 ? NUS_ROWS_F32_CTAS : 4) : NT == 256 ? (sizeof(Real) == 4 ? 3 : 2) : 1) fft_rows_crop_kernel(
     const typename C2<Real>::T* __restrict__ grid, int64_t mr, int R, int C, int RPC, int64_t kpad,
     int k_count, int64_t nc, int64_t mode_offset, const Real* __restrict__ deconv,
     const typename C2<Real>::T* __restrict__ tw_c, typename C2<Real>::T* __restrict__ j_out,
