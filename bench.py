@@ -470,7 +470,10 @@ def main():
     wl = make_workload(args.workload, rank)
     if args.eps is not None:
         wl.eps = args.eps
-    est = _Estimator(wl.times, wl.centers, wl.f_max, float(wl.f_w[0]), wl.k, wl.eps, 1,
+    # independent channels (C3): each channel's tapers on its own grid with its own half-bandwidth
+    # (same time-bandwidth product, so the channels share one DPSS)
+    fw = wl.f_w if np.ndim(wl.times) == 2 and np.size(wl.f_w) == np.shape(wl.times)[0] else float(wl.f_w[0])
+    est = _Estimator(wl.times, wl.centers, wl.f_max, fw, wl.k, wl.eps, 1,
                      wl.precision, local)
     setup = est.setup_ms()
     C_, n, k, nc = est.channels, est.n, est.k, est.nc

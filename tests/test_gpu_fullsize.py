@@ -64,13 +64,14 @@ def _shape_check(w, t, nw, k, tol_dpss, threads=THREADS):
 @pytest.mark.parametrize("kern", ["es"])
 def test_c3_256x2e18_channels_fp32_vs_reference(kern):
     """C3: 256 channels x N = 2^18 (fp32, eps 1e-5, NW 5, K 9, I = 2^17 -> Mr = 2^18: the own two-pass
-    FFT, two taper groups per spread), each channel with its own gaps and its own f_w, against the
+    FFT, the nine tapers as two streaming spread launches), each channel with its own gaps and its own f_w, against the
     reference per channel (host threads across channels)."""
     _need_ref()
     wl = W.c3(channels=256)
     est = nus.api._Estimator(wl.times, wl.centers, wl.f_max, wl.f_w, wl.k, wl.eps, 1, "f32", 0)
     assert est.info.mr == 1 << 18
-    assert est.stage_kernels() == ["spread_tc_kernel", "fft_cols_blk_kernel", "fft_rows_crop_kernel"]  # K = 9: two taper groups
+    # K = 9 in fp32: two streaming spread launches (8 + 1 tapers)
+    assert est.stage_kernels() == ["spread_stream_kernel", "fft_cols_blk_kernel", "fft_rows_crop_kernel"]
     p = est.power(wl.values)
     w = est.tapers()
 

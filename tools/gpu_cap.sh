@@ -3,7 +3,7 @@
 # usage: TAG=r3g KERNELS="fft_cols_blk fft_rows_crop" BARGS="--workload c2" bash tools/gpu_cap.sh
 mkdir -p gpurun_out /tmp/ncu
 T=${TAG:-cap}
-NCU="ncu --set full --import-source on --clock-control none -c 1"
+NCU="ncu -f --set full --import-source on --clock-control none -c 1"
 for re in $KERNELS; do
   name=${re}${SUFFIX}
   timeout 900 $NCU -k regex:$re -s ${SKIP:-3} -o /tmp/ncu/$name python bench.py --no-cpu --steps 2 --warmup 3 --e2e-steps 1 $BARGS > gpurun_out/${T}_$name.log 2>&1
