@@ -533,7 +533,7 @@ def main():
     # step overlap the compute of its neighbours (the same rotation of 4 series as the device leg)
     # up to 100 steps (pipeline fill / drain amortised), host buffers capped at ~2 GB
     step_bytes = C_ * (n + nc) * 8
-    e2e_steps = args.e2e_steps or max(3, min(args.steps, 100, int(2e9 // step_bytes)))
+    e2e_steps = args.e2e_steps or max(3, min(100, int(2e9 // step_bytes)))
     xh = torch.empty((e2e_steps, C_, n), dtype=torch.float64, pin_memory=True).numpy()
     for i in range(e2e_steps):
         xh[i] = np.roll(vals, 17 * (i % nrot), axis=1)
