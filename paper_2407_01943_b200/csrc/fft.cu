@@ -264,7 +264,7 @@ __device__ inline PassATwiddles<T2> pass_a_twiddles(int64_t j2, int out0, int st
 // pipeline.  Rows outside the occupied interval are zeros and are not read.
 // LGR > 0: the column length R = 2^LGR is a compile-time constant (every shared-memory and
 // register-slot index of the in-CTA FFT folds to an immediate); 0 = runtime R.
-template <typename Real, int R0, int NT, int LGR = 0>
+template <typename Real, int R0, int NT, int LGR = 0, int LW = 0>
 __global__ void __launch_bounds__(NT, NT == 128 ? 4 : NT == 256 ? (sizeof(Real) == 4 ? 3 : 2) : 1) fft_cols_blk_kernel(
     const typename C2<Real>::T* __restrict__ grid, typename C2<Real>::T* __restrict__ out, int64_t mr, int R, int C,
     int CW, int k, int kpad, const typename C2<Real>::T* __restrict__ tw_r,
@@ -273,6 +273,7 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 4 : NT == 256 ? (sizeof(Real) 
   using T2 = typename C2<Real>::T;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T2* const buf = reinterpret_cast<T2*>(smem_raw);  // [R][CW]
+  constexpr int lw = LW;  // FusedFft::lw, compile-time
   constexpr int kLgTile = NT == 128 ? 11 : NT == 256 ? 12 : 13;
   if constexpr (LGR > 0) {
     R = 1 << LGR;
@@ -284,7 +285,9 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 4 : NT == 256 ? (sizeof(Real) 
   const int t = blockIdx.x;
   const int blk = t & ((1 << lg_nblk) - 1), ck = t >> lg_nblk;
   const int ch = ck / k, kk = ck - ch * k;
-  const T2* src = grid + (static_cast<int64_t>(ch) * kpad + kk) * mr + (static_cast<int64_t>(blk) << (lgR + lgCW));
+  // tile blk is columns [(blk mod 2^lw) CW, +CW) of layout block blk >> lw, whose rows hold CW << lw cells
+  const T2* src = grid + (static_cast<int64_t>(ch) * kpad + kk) * mr +
+                  (static_cast<int64_t>(blk >> lw) << (lgR + lgCW + lw)) + ((blk & ((1 << lw) - 1)) << lgCW);
   pdl_launch_dependents();
   pdl_wait();  // the spread's grid
   T2 v[16];
@@ -293,7 +296,7 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 4 : NT == 256 ? (sizeof(Real) 
     int f, e;
     stage0_index<R0, NT>(sl, lgR, lgCW, f, e);
     const bool occ = static_cast<unsigned>((e - row_lo) & (R - 1)) < static_cast<unsigned>(row_cnt);
-    v[sl] = occ ? src[e * CW + f] : T2{Real(0), Real(0)};
+    v[sl] = occ ? src[((e * CW) << lw) + f] : T2{Real(0), Real(0)};
   }
   int f, out0, st;
   fft16_regs<R0, false, T2, NT>(v, buf, lgR, lgCW, CW, 1, tw_r, f, out0, st);
@@ -829,12 +832,26 @@ void configure_fft_kernels() {
   NUS_ATTR((fft_cols_blk_kernel<double, 4, kFftThreads, 10>));
   NUS_ATTR((fft_cols_blk_kernel<double, 8, kFftThreads, 11>));
   NUS_ATTR((fft_cols_blk_kernel<double, 16, kFftThreads, 12>));
+  NUS_ATTR((fft_cols_blk_kernel<double, 4, kFftThreads, 10, 1>));
+  NUS_ATTR((fft_cols_blk_kernel<double, 8, kFftThreads, 11, 1>));
+  NUS_ATTR((fft_cols_blk_kernel<double, 8, kFftThreads, 11, 2>));
+  NUS_ATTR((fft_cols_blk_kernel<double, 16, kFftThreads, 12, 1>));
+  NUS_ATTR((fft_cols_blk_kernel<double, 16, kFftThreads, 12, 2>));
+  NUS_ATTR((fft_cols_blk_kernel<double, 16, kFftThreads, 12, 3>));
 #undef NUS_ATTR
   const int smem_w = 2 * kFftElems * static_cast<int>(sizeof(double2));
 #define NUS_ATTRW(KERN) NUS_CUDA(cudaFuncSetAttribute(KERN, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_w))
   NUS_ATTRW((fft_cols_blk_kernel<double, 16, 512>));
   NUS_ATTRW((fft_cols_blk_kernel<float, 16, 512>));
   NUS_ATTRW((fft_cols_blk_kernel<double, 2, 512>));
+  NUS_ATTRW((fft_cols_blk_kernel<double, 16, 512, 0, 1>));
+  NUS_ATTRW((fft_cols_blk_kernel<double, 16, 512, 0, 2>));
+  NUS_ATTRW((fft_cols_blk_kernel<double, 2, 512, 0, 1>));
+  NUS_ATTRW((fft_cols_blk_kernel<double, 2, 512, 0, 2>));
+  NUS_ATTRW((fft_cols_blk_kernel<double, 4, 512>));
+  NUS_ATTRW((fft_cols_blk_kernel<double, 8, 512>));
+  NUS_ATTRW((fft_cols_blk_kernel<float, 4, 512>));
+  NUS_ATTRW((fft_cols_blk_kernel<float, 8, 512>));
   NUS_ATTRW((fft_cols_blk_kernel<float, 2, 512>));
   NUS_ATTRW((fft_rows_crop_kernel<double, double, 2, 512>));
   NUS_ATTRW((fft_rows_crop_kernel<float, float, 2, 512>));
@@ -887,6 +904,10 @@ void fused_fft_prepare(Plan& plan) {
   if (f.cols_mode == 0 && (f.R > kFftElems / 2 || f.R < 32)) f.cols_mode = 1;  // a 2048-cell tile must hold >= 1 column
   if (f.cols_mode == 2 && f.R < 32) f.cols_mode = 1;
   if (wide) f.cols_mode = 3;  // R = 4096 / 8192 rows x CW = 2 / 1 columns per 8192-cell tile
+  {  // NUS_FFT_COLS=wide: 8192-cell tiles (512 threads, 1 CTA/SM) at any R >= 32: twice the columns per tile
+    const char* e = std::getenv("NUS_FFT_COLS");
+    if (e && std::strcmp(e, "wide") == 0 && f.R >= 32) f.cols_mode = 3;
+  }
   if (f.R > 1 && f.R <= 16) f.cols_mode = 4;  // short columns: register DFTs (fft_cols_small_kernel)
   const int tile = f.cols_mode == 0 ? kFftElems / 2 : f.cols_mode == 3 ? 2 * kFftElems : kFftElems;
   f.CW = f.R > 1 ? tile / f.R : 0;
@@ -894,7 +915,26 @@ void fused_fft_prepare(Plan& plan) {
   // blocked grid layout whenever there is a pass A (every pass-A tile contiguous)
   f.blocked = f.R > 1;
   f.lgC = ilog2(f.C);
-  f.lgCW = f.CW > 0 ? ilog2(f.CW) : 0;
+  // fp64 grids with narrow tiles (CW <= 4 columns: R >= 1024): the layout's column blocks are 2^lw = 2
+  // tiles wide, so that the spread's 8-cell stores land in pieces twice as long (CW = 4: one 128-byte
+  // row instead of two 64-byte ones); a pass-A CTA then reads its CW-column slice of the block's rows.
+  // Measured (NUS_FFT_LW = 0 / 1 / 2): C2 spread 74.7 / 71.3 / 71.3 us; C5 spread 333 / 272 / 264 with
+  // pass A 220 / 240 / 258; C4's structure at 2^24 (CW = 1) spread 4.60 / 2.15 / 1.99 ms with pass A
+  // 1.94 / 1.86 / 2.00; full C4 (8192-cell tiles) 17.5 / 16.7 / 16.7 ms per spectrum.
+  f.lw = 0;
+  const bool env_wide = [] {
+    const char* e = std::getenv("NUS_FFT_COLS");
+    return e && std::strcmp(e, "wide") == 0;
+  }();
+  if (p.precision == NUS_F64 && !env_wide &&
+      ((f.cols_mode == 1 && f.R >= 1024 && f.R <= 4096) || (f.cols_mode == 3 && f.R >= 4096))) {
+    const char* e = std::getenv("NUS_FFT_LW");
+    int lw = e ? std::atoi(e) : 1;
+    lw = std::max(0, std::min(lw, f.cols_mode == 3 ? 2 : 3));
+    while (lw > 0 && (f.CW << lw) > 8) --lw;  // instantiated up to 8-column blocks
+    f.lw = lw;
+  }
+  f.lgCW = (f.CW > 0 ? ilog2(f.CW) : 0) + f.lw;
   f.lgT = ilog2(f.R) + f.lgCW;
   const bool f64 = p.precision == NUS_F64;
   const size_t cb = f64 ? sizeof(double2) : sizeof(float2);
@@ -972,19 +1012,47 @@ void launch_cols(const Plan& plan, void* grid, void* scratch, int64_t k, int64_t
   }
   if (f.cols_mode != 2) {
 #define NUS_COLS_REG(R0, NT) NUS_COLS_REGL(R0, NT, 0)
-#define NUS_COLS_REGL(R0, NT, LG)                                                                            \
-  launch_pdl(fft_cols_blk_kernel<Real, R0, NT, LG>, dim3(static_cast<unsigned>(ntiles)), dim3(NT),            \
+#define NUS_COLS_REGL(R0, NT, LG) NUS_COLS_REGW(R0, NT, LG, 0)
+#define NUS_COLS_REGW(R0, NT, LG, LWV)                                                                       \
+  launch_pdl(fft_cols_blk_kernel<Real, R0, NT, LG, LWV>, dim3(static_cast<unsigned>(ntiles)), dim3(NT),       \
              static_cast<size_t>(NT) * 16 * sizeof(T2), s, static_cast<const T2*>(g), out, p.mr, f.R, f.C, f.CW, \
              static_cast<int>(k), static_cast<int>(kpad), tr, th, tl, f.lo_bits, f.row_lo, f.row_cnt)
-    if (f.cols_mode == 3) {  // R = 4096 (Mr = 2^25) or 8192 (2^26)
+    if (f.cols_mode == 3 && f.lw > 0) {  // fp64, R = 4096 / 8192 (fused_fft_prepare)
+      if constexpr (std::is_same_v<Real, double>) {
+        if (r0 == 16 && f.lw == 1) NUS_COLS_REGW(16, 512, 0, 1);
+        else if (r0 == 16 && f.lw == 2) NUS_COLS_REGW(16, 512, 0, 2);
+        else if (r0 == 2 && f.lw == 1) NUS_COLS_REGW(2, 512, 0, 1);
+        else if (r0 == 2 && f.lw == 2) NUS_COLS_REGW(2, 512, 0, 2);
+        else fail(NUS_ERR_INVALID_ARGUMENT, "fft: unsupported layout block width for 8192-element tiles");
+      } else {
+        fail(NUS_ERR_INVALID_ARGUMENT, "fft: wide layout blocks are fp64 only");
+      }
+    } else if (f.cols_mode == 3) {  // R = 4096 (Mr = 2^25) or 8192 (2^26)
       if (r0 == 16) NUS_COLS_REG(16, 512);
       else if (r0 == 2) NUS_COLS_REG(2, 512);
+      else if (r0 == 4) NUS_COLS_REG(4, 512);
+      else if (r0 == 8) NUS_COLS_REG(8, 512);
       else fail(NUS_ERR_INVALID_ARGUMENT, "fft: unexpected first radix for 8192-element tiles");
     } else if (f.cols_mode == 0) {
       if (r0 == 16) NUS_COLS_REG(16, 128);
       else if (r0 == 8) NUS_COLS_REG(8, 128);
       else if (r0 == 4) NUS_COLS_REG(4, 128);
       else NUS_COLS_REG(2, 128);
+    } else if (f.lw > 0) {  // fp64 only (fused_fft_prepare): layout blocks of 2^lw tiles
+      if constexpr (std::is_same_v<Real, double>) {
+        const int key = f.R * 4 + f.lw;
+        switch (key) {
+          case 1024 * 4 + 1: NUS_COLS_REGW(4, kFftThreads, 10, 1); break;
+          case 2048 * 4 + 1: NUS_COLS_REGW(8, kFftThreads, 11, 1); break;
+          case 2048 * 4 + 2: NUS_COLS_REGW(8, kFftThreads, 11, 2); break;
+          case 4096 * 4 + 1: NUS_COLS_REGW(16, kFftThreads, 12, 1); break;
+          case 4096 * 4 + 2: NUS_COLS_REGW(16, kFftThreads, 12, 2); break;
+          case 4096 * 4 + 3: NUS_COLS_REGW(16, kFftThreads, 12, 3); break;
+          default: fail(NUS_ERR_INVALID_ARGUMENT, "fft: unsupported layout block width");
+        }
+      } else {
+        fail(NUS_ERR_INVALID_ARGUMENT, "fft: wide layout blocks are fp64 only");
+      }
     } else {
       switch (f.R) {  // the column lengths of the configs (Mr = 2^17 .. 2^24), compile-time shapes
         case 64: NUS_COLS_REGL(4, kFftThreads, 6); break;
@@ -1003,6 +1071,7 @@ void launch_cols(const Plan& plan, void* grid, void* scratch, int64_t k, int64_t
     }
 #undef NUS_COLS_REG
 #undef NUS_COLS_REGL
+#undef NUS_COLS_REGW
     return;
   }
   const unsigned grid_x = static_cast<unsigned>(std::min<int64_t>(ntiles, sm_count()));

@@ -150,6 +150,9 @@ struct FusedFft {
   // pass-A column block (tile, 2^lgT = R*CW cells) is contiguous; lgC/lgCW/lgT are its shifts
   bool blocked = false;
   int lgC = 0, lgCW = 0, lgT = 12;
+  // lw: the layout's column blocks are 2^lw pass-A tiles wide (lgCW, lgT describe the layout; CW the
+  // tile): a tile is then a CW-column slice of a wider block, whose rows the spread stores in one piece
+  int lw = 0;
   // pass A over the blocked grid: 1 = register-loading tiles of 4096 (256 threads, default),
   // 0 = tiles of 2048 (128 threads), 2 = bulk-copy pipeline (NUS_FFT_COLS=reg128 / async)
   int cols_mode = 1;
